@@ -1,0 +1,205 @@
+"""B200-native hot path of SVFusion (arXiv 2601.08528): batched graph ANNS search / insert / delete on sm_100a.
+
+Thin Python binding over libsvf.so (include/svf.h): argument marshalling only.  PyTorch supplies device memory
+and streams; every step of the method runs in the CUDA kernels under csrc/.  Inputs may be torch tensors (CUDA
+or CPU) or numpy arrays; outputs follow the query's placement (CUDA tensor in -> CUDA tensor out, else numpy).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from ._lib import SENTINEL, SvfError, SvfParams, check, lib  # noqa: F401
+
+try:  # torch is plumbing only (device memory, streams, process groups)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+__all__ = ["Index", "merge_topk", "SvfError", "SENTINEL", "default_params"]
+
+
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _prep(x, np_dtype, torch_dtype):
+    """-> (pointer, keepalive, device or None)"""
+    if _is_torch(x):
+        t = x.detach()
+        if t.dtype != torch_dtype:
+            t = t.to(torch_dtype)
+        t = t.contiguous()
+        return t.data_ptr(), t, (t.device if t.is_cuda else None)
+    a = np.ascontiguousarray(x, dtype=np_dtype)
+    return a.ctypes.data, a, None
+
+
+def _stream(device) -> Optional[int]:
+    if device is None or torch is None:
+        return None
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _empty(shape, np_dtype, torch_dtype, device):
+    if device is not None:
+        t = torch.empty(shape, dtype=torch_dtype, device=device)
+        return t.data_ptr(), t
+    a = np.empty(shape, dtype=np_dtype)
+    return a.ctypes.data, a
+
+
+def default_params(dim: int, degree: int, **kw) -> SvfParams:
+    p = SvfParams()
+    lib().svf_default_params(ctypes.byref(p), dim, degree)
+    metric = kw.pop("metric", 0)
+    p.metric = {"l2": 0, "ip": 1}.get(metric, metric) if isinstance(metric, str) else int(metric)
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown svf_params field {k!r}")
+        setattr(p, k, v)
+    return p
+
+
+class Index:
+    """An SVFusion-style dynamic graph index resident in one GPU's HBM (svf_index*)."""
+
+    def __init__(self, handle: int, params: SvfParams):
+        self._h = ctypes.c_void_p(handle)
+        self.params = params
+        self.device = params.device
+
+    # ---- construction -------------------------------------------------------------------------------------------
+    @classmethod
+    def build(cls, X, degree: int, capacity: Optional[int] = None, **kw) -> "Index":
+        """Build(X_init): exact R-NN seed + batched-insert growth (svf_build)."""
+        ptr, keep, dev = _prep(X, np.float32, torch.float32 if torch else None)
+        n, dim = int(keep.shape[0]), int(keep.shape[1])
+        if dev is not None:
+            kw.setdefault("device", dev.index or 0)
+        p = default_params(dim, degree, capacity=capacity or n, **kw)
+        h = ctypes.c_void_p()
+        check(lib().svf_build(ctypes.byref(p), ptr, n, _stream(dev), ctypes.byref(h)))
+        return cls(h.value, p)
+
+    @classmethod
+    def from_state(cls, vec, graph, edge_dist=None, tomb=None, capacity: Optional[int] = None, **kw) -> "Index":
+        """svf_import: an index from given (vec, graph, edge_dist, tomb) state (tests / bench)."""
+        v = np.ascontiguousarray(vec, dtype=np.float32)
+        g = np.ascontiguousarray(graph, dtype=np.uint32)
+        e = None if edge_dist is None else np.ascontiguousarray(edge_dist, dtype=np.float32)
+        t = None if tomb is None else np.ascontiguousarray(tomb, dtype=np.uint32)
+        n = v.shape[0]
+        p = default_params(v.shape[1], g.shape[1], capacity=capacity or n, **kw)
+        h = ctypes.c_void_p()
+        check(lib().svf_import(ctypes.byref(p), v.ctypes.data, g.ctypes.data, None if e is None else e.ctypes.data,
+                               None if t is None else t.ctypes.data, n, ctypes.byref(h)))
+        return cls(h.value, p)
+
+    # ---- operations ---------------------------------------------------------------------------------------------
+    def search(self, Q, k: int, itopk: int):
+        """Search(q, k) for a batch (svf_search; Algorithm 1).  Returns (ids uint32 [nq,k], dists f32 [nq,k])."""
+        qp, qk, dev = _prep(Q, np.float32, torch.float32 if torch else None)
+        nq = int(qk.shape[0])
+        ip, ids = _empty((nq, k), np.uint32, torch.int32 if torch else None, dev)
+        dp, d = _empty((nq, k), np.float32, torch.float32 if torch else None, dev)
+        check(lib().svf_search(self._h, qp, nq, k, itopk, ip, dp, _stream(dev)))
+        return ids, d
+
+    def insert(self, X):
+        """Insert(x) for a batch (svf_insert).  Returns the assigned ids (numpy uint32)."""
+        xp, xk, dev = _prep(X, np.float32, torch.float32 if torch else None)
+        n = int(xk.shape[0])
+        out = np.empty(n, np.uint32)
+        check(lib().svf_insert(self._h, xp, n, out.ctypes.data, _stream(dev)))
+        return out
+
+    def delete(self, ids) -> int:
+        """Delete(x) for a batch of ids (svf_delete).  Returns the number newly deleted."""
+        ptr, keep, dev = _prep(ids, np.uint32, torch.int32 if torch else None)
+        n = int(keep.numel()) if _is_torch(keep) else int(keep.size)
+        newly = ctypes.c_int64()
+        check(lib().svf_delete(self._h, ptr, n, ctypes.byref(newly), _stream(dev)))
+        return newly.value
+
+    def knn_exact(self, Q, k: int):
+        """Exact k-NN over the live set (svf_knn_exact; ground truth)."""
+        qp, qk, dev = _prep(Q, np.float32, torch.float32 if torch else None)
+        nq = int(qk.shape[0])
+        ip, ids = _empty((nq, k), np.uint32, torch.int32 if torch else None, dev)
+        dp, d = _empty((nq, k), np.float32, torch.float32 if torch else None, dev)
+        check(lib().svf_knn_exact(self._h, qp, nq, k, ip, dp, _stream(dev)))
+        return ids, d
+
+    def link_candidates(self, cand_ids, cand_d, X=None):
+        """TEST ENTRY (svf_link_candidates): steps (ii)+(iii) of insertion from given candidate lists."""
+        ci = np.ascontiguousarray(cand_ids, dtype=np.uint32)
+        cd = np.ascontiguousarray(cand_d, dtype=np.float32)
+        xp = None
+        if X is not None:
+            xk = np.ascontiguousarray(X, dtype=np.float32)
+            xp = xk.ctypes.data
+        check(lib().svf_link_candidates(self._h, xp, ci.ctypes.data, cd.ctypes.data, ci.shape[0], ci.shape[1], None))
+
+    def export(self) -> dict:
+        n = self.info()["n_alloc"]
+        D, R = self.params.dim, self.params.degree
+        vec = np.empty((n, D), np.float32)
+        graph = np.empty((n, R), np.uint32)
+        ed = np.empty((n, R), np.float32)
+        tomb = np.empty(((n + 31) // 32,), np.uint32)
+        na = ctypes.c_int64()
+        check(lib().svf_export(self._h, vec.ctypes.data, graph.ctypes.data, ed.ctypes.data, tomb.ctypes.data,
+                               ctypes.byref(na)))
+        return {"vec": vec, "graph": graph, "edge_dist": ed, "tomb": tomb, "n_alloc": na.value}
+
+    def set_search_params(self, search_width: int = 1, n_init: int = 0, max_iter: int = 0, hash_bits: int = 0):
+        check(lib().svf_set_search_params(self._h, search_width, n_init, max_iter, hash_bits))
+
+    def last_search_counters(self) -> dict:
+        out = (ctypes.c_uint64 * 4)()
+        check(lib().svf_last_search_counters(self._h, out))
+        return {"n_dist": out[0], "iters": out[1], "n_exp": out[2], "queries": out[3]}
+
+    def profile(self, enable: bool = True):
+        check(lib().svf_profile(self._h, int(enable)))
+
+    def profile_read(self) -> dict:
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        check(lib().svf_profile_read(self._h, ms, cnt))
+        names = ["search", "insert_search", "detour", "reverse"]
+        return {n: (ms[i], cnt[i]) for i, n in enumerate(names)}
+
+    def info(self) -> dict:
+        a, d, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib().svf_info(self._h, ctypes.byref(a), ctypes.byref(d), ctypes.byref(c)))
+        return {"n_alloc": a.value, "n_deleted": d.value, "capacity": c.value}
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().svf_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def merge_topk(ids, dists):
+    """K-M (svf_merge_topk): [G, nq, k] CUDA tensors of global ids / dists -> first k per query by (dist, id)."""
+    if not (_is_torch(ids) and ids.is_cuda):
+        raise TypeError("merge_topk takes CUDA tensors (the all-gather output)")
+    G, nq, kk = ids.shape
+    k = kk
+    ids = ids.contiguous()
+    dists = dists.to(torch.float32).contiguous()
+    oi = torch.empty((nq, k), dtype=torch.int32, device=ids.device)
+    od = torch.empty((nq, k), dtype=torch.float32, device=ids.device)
+    check(lib().svf_merge_topk(ids.data_ptr(), dists.data_ptr(), G, nq, kk, oi.data_ptr(), od.data_ptr(),
+                               _stream(ids.device)))
+    return oi, od

@@ -1,0 +1,697 @@
+// libsvf.so: the C ABI of include/svf.h — index state in HBM, host/device staging, validation, error handling.
+// Every step of the method runs in the kernels of search.cu / link.cu / knn.cu; this file only marshals.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/svf.h"
+#include "kernels.h"
+
+using namespace svf;
+
+struct svf_index {
+  svf_params p{};
+  int dev = 0, num_sms = 148;
+  int D = 0, Dp = 0, dq = 0, R = 0, P = 0;
+  int64_t cap = 0, n_alloc = 0, n_deleted = 0;
+  float* vec = nullptr;
+  uint32_t* graph = nullptr;
+  float* edge_dist = nullptr;
+  uint32_t* tomb = nullptr;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  unsigned long long* small = nullptr;  // [0] work counter, [1] newly-deleted, [2] bad flag
+  uint32_t* counters = nullptr;         // [nq][3] of the last search
+  int64_t counters_cap = 0, counters_nq = 0;
+  cudaStream_t last_stream = nullptr;
+  bool poisoned = false;
+  int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
+  bool prof = false;
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_cnt[4] = {0, 0, 0, 0};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+svf_status fail(svf_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+svf_status cuda_fail(svf_index* idx, cudaError_t e, const char* what) {
+  if (idx) idx->poisoned = true;
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  return fail(e == cudaErrorMemoryAllocation ? SVF_ERR_OOM : SVF_ERR_CUDA, buf);
+}
+
+#define CK(idx, expr, what)                                \
+  do {                                                     \
+    cudaError_t e_ = (expr);                               \
+    if (e_ != cudaSuccess) return cuda_fail(idx, e_, what); \
+  } while (0)
+
+bool is_device_ptr(const void* ptr) {
+  if (ptr == nullptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// grow-only scratch; reallocation synchronises the stream first (rare)
+cudaError_t ensure_scratch(svf_index* idx, size_t bytes, cudaStream_t st) {
+  if (bytes <= idx->scratch_bytes) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  if (idx->scratch) cudaFree(idx->scratch);
+  idx->scratch = nullptr;
+  idx->scratch_bytes = 0;
+  size_t want = std::max(bytes, (size_t)64 << 20);
+  e = cudaMalloc(&idx->scratch, want);
+  if (e != cudaSuccess) return e;
+  idx->scratch_bytes = want;
+  return cudaSuccess;
+}
+
+int pow2_at_least(int x) {
+  int v = 1;
+  while (v < x) v <<= 1;
+  return v;
+}
+
+struct SearchCfg {
+  int kpl, cpl, hbits, team, nv, n_init;
+  size_t smem_per_warp;
+};
+
+bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, SearchCfg& c, std::string& why) {
+  if (p < 1 || p > 8) return why = "search_width must be in [1, 8]", false;
+  const int LP = pow2_at_least(std::max(L, 32));
+  const int MP = pow2_at_least(std::max(p * idx->R, 32));
+  if (LP > 512) return why = "itopk must be <= 512", false;
+  if (MP > 256) return why = "search_width * degree must be <= 256", false;
+  c.kpl = LP / 32;
+  c.cpl = MP / 32;
+  int minbits = 1;
+  while ((1 << minbits) < 4 * std::max(LP, MP)) ++minbits;  // forgetful-table invariant (I7)
+  c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(11, minbits);
+  if (c.hbits > 15) return why = "hash_bits too large", false;
+  c.team = pow2_at_least((idx->dq + 3) / 4);
+  c.nv = (idx->dq + c.team - 1) / c.team;
+  c.n_init = n_init > 0 ? n_init : L;
+  c.smem_per_warp = search_smem_per_warp(idx->dq, MP, c.hbits);
+  return true;
+}
+
+// run K-S on the index: Q (device) with row stride q_stride and q_dim valid floats
+cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_dim, int64_t nq, uint64_t n_snapshot,
+                       uint64_t qidx_base, int L, int n_out, const SearchCfg& c, int p, int max_iter,
+                       uint32_t* out_ids, float* out_d, uint32_t* counters, int prof_slot, cudaStream_t st) {
+  SearchArgs a{};
+  a.vec = idx->vec;
+  a.dq = idx->dq;
+  a.graph = idx->graph;
+  a.R = idx->R;
+  a.tomb = idx->n_deleted > 0 ? idx->tomb : nullptr;
+  a.n_alloc = n_snapshot;
+  a.Q = Q;
+  a.q_stride = q_stride;
+  a.q_dim = q_dim;
+  a.nq = nq;
+  a.qidx_base = qidx_base;
+  a.L = L;
+  a.p = p;
+  a.n_init = c.n_init;
+  a.max_iter = max_iter;
+  a.metric = idx->p.metric;
+  a.seed = idx->p.seed;
+  a.team = c.team;
+  a.nv = c.nv;
+  a.hbits = c.hbits;
+  a.n_out = n_out;
+  a.out_ids = out_ids;
+  a.out_d = out_d;
+  a.counters = counters;
+  a.work_counter = idx->small;
+  a.smem_per_warp = c.smem_per_warp;
+  cudaError_t e = cudaMemsetAsync(idx->small, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  if (idx->prof) cudaEventRecord(idx->ev0, st);
+  e = launch_search(a, c.kpl, c.cpl, idx->num_sms, st);
+  if (e != cudaSuccess) return e;
+  if (idx->prof) {
+    cudaEventRecord(idx->ev1, st);
+    cudaEventSynchronize(idx->ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, idx->ev0, idx->ev1);
+    idx->prof_ms[prof_slot] += ms;
+    idx->prof_cnt[prof_slot] += 1;
+  }
+  return cudaSuccess;
+}
+
+template <class F>
+cudaError_t timed(svf_index* idx, int slot, cudaStream_t st, F f) {
+  if (idx->prof) cudaEventRecord(idx->ev0, st);
+  cudaError_t e = f();
+  if (e != cudaSuccess) return e;
+  if (idx->prof) {
+    cudaEventRecord(idx->ev1, st);
+    cudaEventSynchronize(idx->ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, idx->ev0, idx->ev1);
+    idx->prof_ms[slot] += ms;
+    idx->prof_cnt[slot] += 1;
+  }
+  return cudaSuccess;
+}
+
+// copy n rows (dim floats, contiguous, host or device) into vec rows [first, first+n), zero-padded to Dp
+cudaError_t put_rows(svf_index* idx, const float* X, int64_t first, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  float* dst = idx->vec + (size_t)first * idx->Dp;
+  if (X == nullptr) return cudaMemsetAsync(dst, 0, (size_t)n * idx->Dp * 4, st);
+  if (idx->Dp == idx->D) return cudaMemcpyAsync(dst, X, (size_t)n * idx->D * 4, cudaMemcpyDefault, st);
+  cudaError_t e = cudaMemsetAsync(dst, 0, (size_t)n * idx->Dp * 4, st);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy2DAsync(dst, (size_t)idx->Dp * 4, X, (size_t)idx->D * 4, (size_t)idx->D * 4, (size_t)n,
+                           cudaMemcpyDefault, st);
+}
+
+svf_status validate_params(const svf_params* p) {
+  if (!p) return fail(SVF_ERR_INVALID, "params is NULL");
+  if (p->dim < 1 || p->dim > 512) return fail(SVF_ERR_INVALID, "dim must be in [1, 512]");
+  if (p->degree < 2 || p->degree > 128) return fail(SVF_ERR_INVALID, "degree must be in [2, 128]");
+  if (p->metric != SVF_L2 && p->metric != SVF_IP) return fail(SVF_ERR_INVALID, "metric must be SVF_L2 or SVF_IP");
+  if (p->capacity < 1 || p->capacity > 0x7FFFFFFFll) return fail(SVF_ERR_INVALID, "capacity must be in [1, 2^31-1]");
+  if (p->search_width < 1 || p->search_width > 8) return fail(SVF_ERR_INVALID, "search_width must be in [1, 8]");
+  if (p->insert_itopk < 1 || p->insert_itopk > 512) return fail(SVF_ERR_INVALID, "insert_itopk must be in [1, 512]");
+  if (p->protect_prefix < -1 || p->protect_prefix > p->degree) return fail(SVF_ERR_INVALID, "bad protect_prefix");
+  if (p->insert_batch < 1) return fail(SVF_ERR_INVALID, "insert_batch must be >= 1");
+  if (p->seed_size < 1) return fail(SVF_ERR_INVALID, "seed_size must be >= 1");
+  if (p->n_init < 0 || p->max_iter < 0) return fail(SVF_ERR_INVALID, "n_init / max_iter must be >= 0");
+  return SVF_OK;
+}
+
+svf_status alloc_index(const svf_params* p, svf_index** out) {
+  svf_status s = validate_params(p);
+  if (s != SVF_OK) return s;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(SVF_ERR_CUDA, "no CUDA device available (libsvf has no CPU path)");
+  }
+  if (p->device < 0 || p->device >= ndev) return fail(SVF_ERR_INVALID, "device ordinal out of range");
+  DeviceGuard g(p->device);
+  svf_index* idx = new svf_index();
+  idx->p = *p;
+  idx->dev = p->device;
+  cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  idx->D = p->dim;
+  idx->Dp = (p->dim + 3) / 4 * 4;
+  idx->dq = idx->Dp / 4;
+  idx->R = p->degree;
+  idx->P = p->protect_prefix < 0 ? p->degree / 2 : p->protect_prefix;
+  idx->cap = p->capacity;
+  idx->search_width = p->search_width;
+  idx->n_init = p->n_init;
+  idx->max_iter = p->max_iter;
+  idx->hash_bits = p->hash_bits;
+  cudaError_t e;
+  const size_t cap = (size_t)idx->cap;
+  if ((e = cudaMalloc(&idx->vec, cap * idx->Dp * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&idx->graph, cap * idx->R * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&idx->edge_dist, cap * idx->R * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&idx->tomb, (cap + 31) / 32 * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&idx->small, 64)) != cudaSuccess ||
+      (e = cudaMemset(idx->tomb, 0, (cap + 31) / 32 * 4)) != cudaSuccess ||
+      (e = cudaEventCreate(&idx->ev0)) != cudaSuccess || (e = cudaEventCreate(&idx->ev1)) != cudaSuccess) {
+    svf_destroy(idx);
+    return cuda_fail(nullptr, e, "allocating the index arenas");
+  }
+  *out = idx;
+  return SVF_OK;
+}
+
+// insertion of rows [n_alloc, n_alloc + n) already present in vec (sub-batch snapshots, I13)
+svf_status insert_present_rows(svf_index* idx, int64_t n, cudaStream_t st) {
+  const int L = idx->p.insert_itopk;
+  SearchCfg c;
+  std::string why;
+  if (!search_cfg(idx, L, idx->p.search_width, idx->p.n_init, idx->hash_bits, c, why))
+    return fail(SVF_ERR_INVALID, why);
+  const int64_t B = std::min<int64_t>(idx->p.insert_batch, std::max<int64_t>(n, 1));
+  const size_t cand_bytes = al((size_t)B * L * 4);
+  const size_t rev_bytes = reverse_scratch_bytes(B, idx->R);
+  CK(idx, ensure_scratch(idx, 2 * cand_bytes + al(rev_bytes), st), "allocating insert scratch");
+  uint32_t* cid = static_cast<uint32_t*>(idx->scratch);
+  float* cd = reinterpret_cast<float*>(static_cast<char*>(idx->scratch) + cand_bytes);
+  void* rev = static_cast<char*>(idx->scratch) + 2 * cand_bytes;
+  CK(idx, launch_fill_rows(idx->graph, idx->edge_dist, idx->n_alloc, n, idx->R, st), "fill rows");
+  int64_t done = 0;
+  while (done < n) {
+    const int64_t snap = idx->n_alloc + done;
+    const int64_t bsz = std::min<int64_t>({(int64_t)idx->p.insert_batch, snap, n - done});
+    // (i) insert-mode search over the snapshot: the sub-batch's own rows are neither reachable nor sampled
+    CK(idx,
+       run_search(idx, idx->vec + (size_t)snap * idx->Dp, idx->Dp, idx->Dp, bsz, (uint64_t)snap, (uint64_t)snap, L,
+                  L, c, idx->p.search_width, idx->p.max_iter, cid, cd, nullptr, 1, st),
+       "insert search");
+    // (ii) detour-ranked forward rows
+    CK(idx, timed(idx, 2, st, [&] {
+         return launch_detour_select(idx->graph, idx->edge_dist, idx->R, idx->P, snap, bsz, cid, cd, L, st);
+       }), "detour select");
+    // (iii) reverse edges
+    CK(idx, timed(idx, 3, st, [&] {
+         return launch_reverse(idx->graph, idx->edge_dist, idx->n_deleted > 0 ? idx->tomb : nullptr, idx->R, idx->P,
+                               snap, bsz, rev, idx->scratch_bytes - 2 * cand_bytes, st);
+       }), "reverse edges");
+    done += bsz;
+  }
+  idx->n_alloc += n;
+  return SVF_OK;
+}
+
+svf_status enter(svf_index* idx) {
+  if (!idx) return fail(SVF_ERR_INVALID, "index is NULL");
+  if (idx->poisoned) return fail(SVF_ERR_POISONED, "index poisoned by an earlier CUDA failure");
+  return SVF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void svf_default_params(svf_params* p, int32_t dim, int32_t degree) {
+  std::memset(p, 0, sizeof *p);
+  p->dim = dim;
+  p->degree = degree;
+  p->metric = SVF_L2;
+  p->capacity = 0;
+  p->search_width = 1;
+  p->n_init = 0;
+  p->max_iter = 0;
+  p->insert_itopk = 128;
+  p->protect_prefix = -1;
+  p->insert_batch = 4096;
+  p->seed_size = 4096;
+  p->hash_bits = 0;
+  p->seed = 42;
+  p->device = 0;
+}
+
+const char* svf_last_error(void) { return g_err.c_str(); }
+
+svf_status svf_build(const svf_params* p, const float* X, int64_t n, void* stream, svf_index** out) {
+  if (!out || !X) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (n < 1) return fail(SVF_ERR_INVALID, "svf_build needs n >= 1");
+  if (p && p->capacity < n) return fail(SVF_ERR_CAPACITY, "capacity < n");
+  svf_index* idx = nullptr;
+  svf_status s = alloc_index(p, &idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto bail = [&](svf_status s2) {
+    svf_destroy(idx);
+    return s2;
+  };
+  if (put_rows(idx, X, 0, n, st) != cudaSuccess) return bail(cuda_fail(nullptr, cudaGetLastError(), "copy X"));
+  // seed: exact R-NN of the first n0 rows (self excluded), written straight into the rows (prefix|tail layout)
+  const int64_t n0 = std::min<int64_t>(n, idx->p.seed_size);
+  const size_t kb = knn_scratch_bytes(n0, idx->R, n0);
+  if (ensure_scratch(idx, kb, st) != cudaSuccess) return bail(cuda_fail(nullptr, cudaGetLastError(), "scratch"));
+  cudaError_t e = launch_knn_exact(idx->vec, idx->dq, n0, nullptr, idx->vec, idx->Dp, idx->Dp, n0, idx->R,
+                                   idx->p.metric, 0, idx->graph, idx->edge_dist, idx->scratch, idx->scratch_bytes,
+                                   idx->num_sms, st);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "seed exact R-NN"));
+  idx->n_alloc = n0;
+  if (n > n0) {
+    s = insert_present_rows(idx, n - n0, st);
+    if (s != SVF_OK) return bail(s);
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(nullptr, e, "build"));
+  *out = idx;
+  return SVF_OK;
+}
+
+svf_status svf_import(const svf_params* p, const float* vec, const uint32_t* graph, const float* edge_dist,
+                      const uint32_t* tomb, int64_t n_alloc, svf_index** out) {
+  if (!out || !vec || !graph) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (n_alloc < 0 || (p && n_alloc > p->capacity)) return fail(SVF_ERR_CAPACITY, "n_alloc > capacity");
+  svf_index* idx = nullptr;
+  svf_status s = alloc_index(p, &idx);
+  if (s != SVF_OK) return s;
+  DeviceGuard g(idx->dev);
+  cudaError_t e;
+  const size_t nr = (size_t)n_alloc * idx->R;
+  if ((e = put_rows(idx, vec, 0, n_alloc, nullptr)) != cudaSuccess ||
+      (e = cudaMemcpy(idx->graph, graph, nr * 4, cudaMemcpyDefault)) != cudaSuccess) {
+    svf_destroy(idx);
+    return cuda_fail(nullptr, e, "import copy");
+  }
+  if (edge_dist) {
+    e = cudaMemcpy(idx->edge_dist, edge_dist, nr * 4, cudaMemcpyDefault);
+  } else {
+    std::vector<float> inf(nr, __builtin_inff());
+    e = cudaMemcpy(idx->edge_dist, inf.data(), nr * 4, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && tomb) {
+    const size_t words = ((size_t)n_alloc + 31) / 32;
+    std::vector<uint32_t> h(words);
+    e = cudaMemcpy(h.data(), tomb, words * 4, cudaMemcpyDefault);
+    if (e == cudaSuccess) {
+      if (n_alloc % 32) h[words - 1] &= (1u << (n_alloc % 32)) - 1u;
+      int64_t cnt = 0;
+      for (uint32_t w : h) cnt += __builtin_popcount(w);
+      idx->n_deleted = cnt;
+      e = cudaMemcpy(idx->tomb, h.data(), words * 4, cudaMemcpyHostToDevice);
+    }
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    svf_destroy(idx);
+    return cuda_fail(nullptr, e, "import copy");
+  }
+  idx->n_alloc = n_alloc;
+  *out = idx;
+  return SVF_OK;
+}
+
+svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int32_t itopk, uint32_t* out_ids,
+                      float* out_dists, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (nq < 0) return fail(SVF_ERR_INVALID, "nq < 0");
+  if (nq == 0) return SVF_OK;
+  if (!Q || !out_ids || !out_dists) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (k < 1 || itopk < k) return fail(SVF_ERR_INVALID, "need 1 <= k <= itopk");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SearchCfg c;
+  std::string why;
+  if (!search_cfg(idx, itopk, idx->search_width, idx->n_init, idx->hash_bits, c, why))
+    return fail(SVF_ERR_INVALID, why);
+  const bool q_dev = is_device_ptr(Q), i_dev = is_device_ptr(out_ids), d_dev = is_device_ptr(out_dists);
+  const size_t qb = q_dev ? 0 : al((size_t)nq * idx->D * 4);
+  const size_t ob = al((size_t)nq * k * 4);
+  CK(idx, ensure_scratch(idx, qb + 2 * ob, st), "search scratch");
+  char* sp = static_cast<char*>(idx->scratch);
+  const float* Qd = Q;
+  if (!q_dev) {
+    CK(idx, cudaMemcpyAsync(sp, Q, (size_t)nq * idx->D * 4, cudaMemcpyHostToDevice, st), "H2D queries");
+    Qd = reinterpret_cast<const float*>(sp);
+  }
+  uint32_t* oi = i_dev ? out_ids : reinterpret_cast<uint32_t*>(sp + qb);
+  float* od = d_dev ? out_dists : reinterpret_cast<float*>(sp + qb + ob);
+  if (idx->counters_cap < nq) {
+    if (idx->counters) cudaFree(idx->counters);
+    idx->counters = nullptr;
+    idx->counters_cap = 0;
+    CK(idx, cudaMalloc(&idx->counters, (size_t)nq * 3 * 4), "counters");
+    idx->counters_cap = nq;
+  }
+  idx->counters_nq = nq;
+  idx->last_stream = st;
+  CK(idx,
+     run_search(idx, Qd, idx->D, idx->D, nq, (uint64_t)idx->n_alloc, 0, itopk, k, c, idx->search_width,
+                idx->max_iter, oi, od, idx->counters, 0, st),
+     "search kernel");
+  if (!i_dev) CK(idx, cudaMemcpyAsync(out_ids, oi, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+  if (!d_dev) CK(idx, cudaMemcpyAsync(out_dists, od, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+  if (!i_dev || !d_dev) CK(idx, cudaStreamSynchronize(st), "search sync");
+  return SVF_OK;
+}
+
+svf_status svf_insert(svf_index* idx, const float* X, int64_t n, uint32_t* out_ids, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (n < 0) return fail(SVF_ERR_INVALID, "n < 0");
+  if (n == 0) return SVF_OK;
+  if (!X) return fail(SVF_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  if (idx->n_alloc < 1) return fail(SVF_ERR_INVALID, "insert into an empty index (build it first)");
+  if (idx->n_alloc + n > idx->cap) return fail(SVF_ERR_CAPACITY, "n_alloc + n > capacity");
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t first = idx->n_alloc;
+  CK(idx, put_rows(idx, X, first, n, st), "copy X");
+  s = insert_present_rows(idx, n, st);
+  if (s != SVF_OK) return s;
+  if (out_ids) {
+    std::vector<uint32_t> h((size_t)n);
+    for (int64_t i = 0; i < n; ++i) h[i] = (uint32_t)(first + i);
+    CK(idx, cudaMemcpyAsync(out_ids, h.data(), (size_t)n * 4, cudaMemcpyDefault, st), "ids");
+    CK(idx, cudaStreamSynchronize(st), "insert sync");
+  }
+  return SVF_OK;
+}
+
+svf_status svf_delete(svf_index* idx, const uint32_t* ids, int64_t n, int64_t* n_newly_deleted, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (n < 0) return fail(SVF_ERR_INVALID, "n < 0");
+  if (n_newly_deleted) *n_newly_deleted = 0;
+  if (n == 0) return SVF_OK;
+  if (!ids) return fail(SVF_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint32_t* d_ids = ids;
+  if (!is_device_ptr(ids)) {
+    CK(idx, ensure_scratch(idx, al((size_t)n * 4), st), "delete scratch");
+    CK(idx, cudaMemcpyAsync(idx->scratch, ids, (size_t)n * 4, cudaMemcpyHostToDevice, st), "H2D ids");
+    d_ids = static_cast<const uint32_t*>(idx->scratch);
+  }
+  unsigned long long* newly = idx->small + 1;
+  unsigned int* bad = reinterpret_cast<unsigned int*>(idx->small + 2);
+  CK(idx, cudaMemsetAsync(idx->small + 1, 0, 16, st), "memset");
+  CK(idx, launch_tomb_check(d_ids, n, (uint64_t)idx->n_alloc, bad, st), "tomb check");
+  unsigned int hbad = 0;
+  CK(idx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st), "D2H");
+  CK(idx, cudaStreamSynchronize(st), "delete sync");
+  if (hbad) return fail(SVF_ERR_NOT_FOUND, "delete of an id >= n_alloc (nothing deleted)");
+  CK(idx, timed(idx, 3, st, [&] { return launch_tomb_set(d_ids, n, idx->tomb, newly, st); }), "tomb set");
+  unsigned long long hn = 0;
+  CK(idx, cudaMemcpyAsync(&hn, newly, 8, cudaMemcpyDeviceToHost, st), "D2H");
+  CK(idx, cudaStreamSynchronize(st), "delete sync");
+  idx->n_deleted += (int64_t)hn;
+  if (n_newly_deleted) *n_newly_deleted = (int64_t)hn;
+  return SVF_OK;
+}
+
+svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, uint32_t* out_ids,
+                         float* out_dists, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (nq < 0 || k < 1 || k > 256) return fail(SVF_ERR_INVALID, "need nq >= 0 and 1 <= k <= 256");
+  if (nq == 0) return SVF_OK;
+  if (!Q || !out_ids || !out_dists) return fail(SVF_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool q_dev = is_device_ptr(Q), i_dev = is_device_ptr(out_ids), d_dev = is_device_ptr(out_dists);
+  const size_t qb = q_dev ? 0 : al((size_t)nq * idx->D * 4);
+  const size_t ob = al((size_t)nq * k * 4);
+  const size_t kb = al(knn_scratch_bytes(nq, k, std::max<int64_t>(idx->n_alloc, 1)));
+  CK(idx, ensure_scratch(idx, qb + 2 * ob + kb, st), "knn scratch");
+  char* sp = static_cast<char*>(idx->scratch);
+  const float* Qd = Q;
+  if (!q_dev) {
+    CK(idx, cudaMemcpyAsync(sp, Q, (size_t)nq * idx->D * 4, cudaMemcpyHostToDevice, st), "H2D queries");
+    Qd = reinterpret_cast<const float*>(sp);
+  }
+  uint32_t* oi = i_dev ? out_ids : reinterpret_cast<uint32_t*>(sp + qb);
+  float* od = d_dev ? out_dists : reinterpret_cast<float*>(sp + qb + ob);
+  CK(idx,
+     launch_knn_exact(idx->vec, idx->dq, idx->n_alloc, idx->n_deleted > 0 ? idx->tomb : nullptr, Qd, idx->D, idx->D,
+                      nq, k, idx->p.metric, -1, oi, od, sp + qb + 2 * ob, idx->scratch_bytes - qb - 2 * ob,
+                      idx->num_sms, st),
+     "knn kernel");
+  if (!i_dev) CK(idx, cudaMemcpyAsync(out_ids, oi, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
+  if (!d_dev) CK(idx, cudaMemcpyAsync(out_dists, od, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+  if (!i_dev || !d_dev) CK(idx, cudaStreamSynchronize(st), "knn sync");
+  return SVF_OK;
+}
+
+svf_status svf_merge_topk(const uint32_t* ids, const float* dists, int32_t G, int64_t nq, int32_t k,
+                          uint32_t* out_ids, float* out_dists, void* stream) {
+  if (G < 1 || nq < 0 || k < 1 || k > 256) return fail(SVF_ERR_INVALID, "need G >= 1, nq >= 0, 1 <= k <= 256");
+  if (nq == 0) return SVF_OK;
+  if (!ids || !dists || !out_ids || !out_dists) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (!is_device_ptr(ids) || !is_device_ptr(dists) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+    return fail(SVF_ERR_INVALID, "svf_merge_topk takes device pointers (the all-gather output)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_merge_topk(ids, dists, G, nq, k, out_ids, out_dists, st);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "merge kernel");
+  return SVF_OK;
+}
+
+svf_status svf_export(const svf_index* cidx, float* vec, uint32_t* graph, float* edge_dist, uint32_t* tomb,
+                      int64_t* n_alloc) {
+  svf_index* idx = const_cast<svf_index*>(cidx);
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  CK(idx, cudaDeviceSynchronize(), "sync");
+  const int64_t n = idx->n_alloc;
+  if (n_alloc) *n_alloc = n;
+  if (vec && n > 0)
+    CK(idx, cudaMemcpy2D(vec, (size_t)idx->D * 4, idx->vec, (size_t)idx->Dp * 4, (size_t)idx->D * 4, (size_t)n,
+                         cudaMemcpyDefault), "export vec");
+  if (graph && n > 0) CK(idx, cudaMemcpy(graph, idx->graph, (size_t)n * idx->R * 4, cudaMemcpyDefault), "export graph");
+  if (edge_dist && n > 0)
+    CK(idx, cudaMemcpy(edge_dist, idx->edge_dist, (size_t)n * idx->R * 4, cudaMemcpyDefault), "export edge_dist");
+  if (tomb && n > 0) CK(idx, cudaMemcpy(tomb, idx->tomb, ((size_t)n + 31) / 32 * 4, cudaMemcpyDefault), "export tomb");
+  return SVF_OK;
+}
+
+svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* cand_ids, const float* cand_d,
+                               int64_t n_new, int32_t n_cand, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (n_new < 0 || n_cand < 1 || n_cand > 512) return fail(SVF_ERR_INVALID, "need n_new >= 0, 1 <= n_cand <= 512");
+  if (n_new == 0) return SVF_OK;
+  if (!cand_ids || !cand_d) return fail(SVF_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  if (idx->n_alloc + n_new > idx->cap) return fail(SVF_ERR_CAPACITY, "n_alloc + n_new > capacity");
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t m = (size_t)n_new * n_cand;
+  std::vector<uint32_t> hid(m);
+  CK(idx, cudaMemcpy(hid.data(), cand_ids, m * 4, cudaMemcpyDefault), "copy candidates");
+  for (uint32_t v : hid)
+    if (v != SVF_SENTINEL && (int64_t)v >= idx->n_alloc)
+      return fail(SVF_ERR_INVALID, "candidate id >= n_alloc (candidates must be existing vertices)");
+  const size_t cb = al(m * 4);
+  const size_t rev = reverse_scratch_bytes(n_new, idx->R);
+  CK(idx, ensure_scratch(idx, 2 * cb + al(rev), st), "link scratch");
+  char* sp = static_cast<char*>(idx->scratch);
+  CK(idx, cudaMemcpyAsync(sp, hid.data(), m * 4, cudaMemcpyHostToDevice, st), "H2D");
+  CK(idx, cudaMemcpyAsync(sp + cb, cand_d, m * 4, cudaMemcpyDefault, st), "H2D");
+  const int64_t first = idx->n_alloc;
+  CK(idx, put_rows(idx, X, first, n_new, st), "copy X");
+  CK(idx, launch_fill_rows(idx->graph, idx->edge_dist, first, n_new, idx->R, st), "fill rows");
+  CK(idx,
+     launch_detour_select(idx->graph, idx->edge_dist, idx->R, idx->P, first, n_new,
+                          reinterpret_cast<uint32_t*>(sp), reinterpret_cast<float*>(sp + cb), n_cand, st),
+     "detour select");
+  CK(idx,
+     launch_reverse(idx->graph, idx->edge_dist, idx->n_deleted > 0 ? idx->tomb : nullptr, idx->R, idx->P, first,
+                    n_new, sp + 2 * cb, idx->scratch_bytes - 2 * cb, st),
+     "reverse edges");
+  CK(idx, cudaStreamSynchronize(st), "link sync");
+  idx->n_alloc += n_new;
+  return SVF_OK;
+}
+
+svf_status svf_set_search_params(svf_index* idx, int32_t search_width, int32_t n_init, int32_t max_iter,
+                                 int32_t hash_bits) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (search_width < 1 || search_width > 8 || n_init < 0 || max_iter < 0 || hash_bits < 0 || hash_bits > 15)
+    return fail(SVF_ERR_INVALID, "bad search params");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->search_width = search_width;
+  idx->n_init = n_init;
+  idx->max_iter = max_iter;
+  idx->hash_bits = hash_bits;
+  return SVF_OK;
+}
+
+svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  out[0] = out[1] = out[2] = 0;
+  out[3] = (uint64_t)idx->counters_nq;
+  if (idx->counters_nq == 0) return SVF_OK;
+  CK(idx, cudaStreamSynchronize(idx->last_stream), "sync");
+  std::vector<uint32_t> h((size_t)idx->counters_nq * 3);
+  CK(idx, cudaMemcpy(h.data(), idx->counters, h.size() * 4, cudaMemcpyDeviceToHost), "D2H counters");
+  for (int64_t q = 0; q < idx->counters_nq; ++q) {
+    out[0] += h[q * 3 + 0];
+    out[1] += h[q * 3 + 1];
+    out[2] += h[q * 3 + 2];
+  }
+  return SVF_OK;
+}
+
+svf_status svf_profile(svf_index* idx, int32_t enable) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->prof = enable != 0;
+  for (int i = 0; i < 4; ++i) {
+    idx->prof_ms[i] = 0;
+    idx->prof_cnt[i] = 0;
+  }
+  return SVF_OK;
+}
+
+svf_status svf_profile_read(svf_index* idx, double ms[4], int64_t cnt[4]) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  for (int i = 0; i < 4; ++i) {
+    ms[i] = idx->prof_ms[i];
+    cnt[i] = idx->prof_cnt[i];
+  }
+  return SVF_OK;
+}
+
+svf_status svf_info(const svf_index* idx, int64_t* n_alloc, int64_t* n_deleted, int64_t* capacity) {
+  if (!idx) return fail(SVF_ERR_INVALID, "index is NULL");
+  if (n_alloc) *n_alloc = idx->n_alloc;
+  if (n_deleted) *n_deleted = idx->n_deleted;
+  if (capacity) *capacity = idx->cap;
+  return SVF_OK;
+}
+
+svf_status svf_destroy(svf_index* idx) {
+  if (!idx) return SVF_OK;
+  DeviceGuard g(idx->dev);
+  cudaDeviceSynchronize();
+  cudaFree(idx->vec);
+  cudaFree(idx->graph);
+  cudaFree(idx->edge_dist);
+  cudaFree(idx->tomb);
+  cudaFree(idx->small);
+  cudaFree(idx->scratch);
+  cudaFree(idx->counters);
+  if (idx->ev0) cudaEventDestroy(idx->ev0);
+  if (idx->ev1) cudaEventDestroy(idx->ev1);
+  cudaGetLastError();
+  delete idx;
+  return SVF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Internal launchers of libsvf.so (below the C ABI in include/svf.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace svf {
+
+constexpr int kSearchWarpsPerBlock = 4;
+
+struct SearchArgs {
+  const float* vec;        // [cap][dq*4]
+  int dq;                  // float4 per row (Dp / 4)
+  const uint32_t* graph;   // [cap][R]
+  int R;
+  const uint32_t* tomb;    // nullable (no deletions)
+  uint64_t n_alloc;        // snapshot: ids >= n_alloc are not sampled nor followed
+  const float* Q;          // query rows
+  int64_t q_stride;        // floats between query rows
+  int q_dim;               // valid floats per query row (zero-padded to dq*4)
+  int64_t nq;
+  uint64_t qidx_base;      // query i seeds its entry points with qidx_base + i (I18)
+  int L, p, n_init, max_iter, metric;
+  uint64_t seed;
+  int team, nv;            // lanes per distance, float4 per lane (team * nv >= dq, nv <= 4)
+  int hbits;               // visited table slots = 2^hbits per warp
+  int n_out;               // k (search) or L (insert mode)
+  uint32_t* out_ids;
+  float* out_d;
+  uint32_t* counters;      // nullable: [nq][3] = n_dist, iters, n_exp
+  unsigned long long* work_counter;  // zeroed before launch
+  size_t smem_per_warp;
+};
+
+size_t search_smem_per_warp(int dq, int mp, int hbits);
+cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
+
+// K-L1: detour-ranked forward rows for new ids [first, first + n_new) from candidates [n_new][nc]
+// (reads the snapshot rows of the candidates, writes rows first..first+n_new-1; disjoint by construction)
+cudaError_t launch_detour_select(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
+                                 const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st);
+// K-L2: reverse edges.  Scratch must hold 2*n_new*R u32 + 2*n_new*R u64 + n_new*R u32 + cub temp bytes.
+size_t reverse_scratch_bytes(int64_t n_new, int R);
+cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R, int P, int64_t first,
+                           int64_t n_new, void* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// K-D: tombstones.  check pass: *bad = 1 if any id >= n_alloc.  set pass: *newly += newly set bits.
+cudaError_t launch_tomb_check(const uint32_t* ids, int64_t n, uint64_t n_alloc, unsigned int* bad, cudaStream_t st);
+cudaError_t launch_tomb_set(const uint32_t* ids, int64_t n, uint32_t* tomb, unsigned long long* newly,
+                            cudaStream_t st);
+
+// K-G (+K-R): exact k-NN over ids [0, n) of vec (live only).  self_base >= 0 excludes id == self_base + query.
+size_t knn_scratch_bytes(int64_t nq, int k, int64_t n);
+cudaError_t launch_knn_exact(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
+                             int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
+                             uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
+                             cudaStream_t st);
+
+// K-M: merge G lists [G][nq][k] (ids/dists) -> first k per query by (dist, id)
+cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
+                              float* out_d, cudaStream_t st);
+
+// small helpers
+cudaError_t launch_pad_rows(const float* src, int64_t n, int dim, float* dst, int dq, cudaStream_t st);
+cudaError_t launch_fill_rows(uint32_t* graph, float* edge_dist, int64_t first, int64_t n, int R, cudaStream_t st);
+cudaError_t launch_unpad_rows(const float* src, int64_t n, int dq, float* dst, int dim, cudaStream_t st);
+
+}  // namespace svf

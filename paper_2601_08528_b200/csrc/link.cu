@@ -1,0 +1,372 @@
+// K-L1 (detour select) and K-L2 (reverse edges): steps (ii) and (iii) of batched insertion (
+// paper §5.1).  The paper runs both on the CPU with atomics + thread-local buffers;
+// here both are GPU kernels and the reverse step is sort-then-apply, which makes it deterministic and equal to
+// the order-independent definition "tail(u) <- first (R-P) of sort_eff(tail(u) U requests(u))" (reading I12).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svf {
+
+namespace {
+
+constexpr int kLinkWarps = 4;
+
+__device__ __forceinline__ int map_find(const uint32_t* mid, const uint16_t* mpos, int mbits, uint32_t id) {
+  const uint32_t mask = (1u << mbits) - 1u;
+  uint32_t h = (id * 0x9E3779B1u) >> (32 - mbits);
+  for (;;) {
+    const uint32_t v = mid[h];
+    if (v == id) return mpos[h];
+    if (v == kSent) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+// One warp per new vertex v = first + b.  Candidate list C = cand_ids[b][0..m) (distance order, SENT-padded).
+// count(i) = |{ j < i : C[i] in row(C[j]) }| ("detourable paths"); stable sort by (count, i) (I11);
+// select the first min(R, m): prefix [0,P) in detour order, tail [P,R) sorted by key(d, id) (I12).
+template <int E>
+__global__ void __launch_bounds__(kLinkWarps * 32)
+    detour_select_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist, int R, int P, int64_t first,
+                         int64_t n_new, const uint32_t* __restrict__ cand_ids, const float* __restrict__ cand_d,
+                         int nc, int mbits) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int M = 1 << mbits;
+  const size_t per_warp = (size_t)nc * 4 + (size_t)nc * 4 + (size_t)M * 4 + (size_t)M * 2 + 16;
+  unsigned char* base = smem + ((per_warp + 15) & ~(size_t)15) * wib;
+  uint32_t* sC = reinterpret_cast<uint32_t*>(base);
+  uint32_t* cnt = sC + nc;
+  uint32_t* mid = cnt + nc;
+  uint16_t* mpos = reinterpret_cast<uint16_t*>(mid + M);
+  const int64_t b = (int64_t)blockIdx.x * kLinkWarps + wib;
+  if (b >= n_new) return;
+  const uint32_t* C = cand_ids + b * nc;
+  const float* Cd = cand_d + b * nc;
+
+  for (int i = lane; i < M; i += 32) mid[i] = kSent;
+  int m = nc;
+  for (int i0 = 0; i0 < nc; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t c = i < nc ? C[i] : kSent;
+    const unsigned s = __ballot_sync(0xffffffffu, i < nc && c == kSent);
+    if (s) {
+      m = i0 + __ffs(s) - 1;
+      break;
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {
+    const uint32_t c = C[i];
+    sC[i] = c;
+    cnt[i] = 0;
+    uint32_t h = (c * 0x9E3779B1u) >> (32 - mbits);
+    while (atomicCAS(mid + h, kSent, c) != kSent) h = (h + 1) & (uint32_t)(M - 1);
+    mpos[h] = (uint16_t)i;
+  }
+  __syncwarp();
+  // detour counts over the snapshot rows of C[0..m-1]
+  const int total = m * R;
+  for (int f0 = 0; f0 < total; f0 += 32 * 4) {
+    uint32_t u[4];
+    int jj[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int f = f0 + t * 32 + lane;
+      jj[t] = f / R;
+      u[t] = f < total ? __ldg(graph + (size_t)sC[jj[t]] * R + (f - jj[t] * R)) : kSent;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (u[t] != kSent) {
+        const int i = map_find(mid, mpos, mbits, u[t]);
+        if (i > jj[t]) atomicAdd(cnt + i, 1u);
+      }
+    }
+  }
+  __syncwarp();
+  uint64_t key[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int i = r * 32 + lane;
+    key[r] = i < m ? (((uint64_t)cnt[i] << 32) | (uint32_t)i) : kEmptyKey;
+  }
+  warp_sort<E>(key, lane);  // (count, i) ascending == stable sort by count
+  const int sel = min(R, m);
+  const int npre = min(P, sel);
+  uint32_t* row = graph + (size_t)(first + b) * R;
+  float* rowd = edge_dist + (size_t)(first + b) * R;
+  for (int s = lane; s < R; s += 32) {
+    row[s] = kSent;
+    rowd[s] = __int_as_float(0x7F800000);
+  }
+  __syncwarp();
+  // prefix: detour order; remaining selected entries staged (as (d,id) keys) for the tail sort
+  uint64_t* tkeys = reinterpret_cast<uint64_t*>(mid);  // reuse the map storage (M*4 >= 2*nc*... >= 8*R)
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int e = r * 32 + lane;
+    if (e < sel) {
+      const int i = (int)(uint32_t)key[r];
+      if (e < npre) {
+        row[e] = sC[i];
+        rowd[e] = Cd[i];
+      } else {
+        tkeys[e - npre] = make_key(Cd[i], sC[i]);
+      }
+    }
+  }
+  __syncwarp();
+  const int ntail = sel - npre;
+  uint64_t tk[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = r * 32 + lane;
+    tk[r] = e < ntail ? tkeys[e] : kEmptyKey;
+  }
+  warp_sort<4>(tk, lane);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = r * 32 + lane;
+    if (e < ntail) {
+      row[P + e] = key_id(tk[r]);
+      rowd[P + e] = key_dist(tk[r]);
+    }
+  }
+}
+
+// Reverse requests (u, key(d, v)) for every forward edge v -> u of the sub-batch.
+__global__ void reverse_emit_kernel(const uint32_t* __restrict__ graph, const float* __restrict__ edge_dist, int R,
+                                    int64_t first, int64_t n_new, uint32_t* __restrict__ ku,
+                                    uint64_t* __restrict__ kv) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_new * R) return;
+  const int64_t b = t / R;
+  const uint32_t v = (uint32_t)(first + b);
+  const uint32_t u = graph[(size_t)v * R + (t - b * R)];
+  ku[t] = u;
+  kv[t] = u == kSent ? kEmptyKey : make_key(edge_dist[(size_t)v * R + (t - b * R)], v);
+}
+
+__global__ void segment_heads_kernel(const uint32_t* __restrict__ ku, int64_t n, uint32_t* __restrict__ heads,
+                                     unsigned int* __restrict__ nseg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t u = ku[i];
+  if (u != kSent && (i == 0 || ku[i - 1] != u)) heads[atomicAdd(nseg, 1u)] = (uint32_t)i;
+}
+
+// One warp per target u: tail(u) <- first (R-P) of sort_eff(tail(u) U requests(u)); prefix untouched; rows of
+// deleted u are frozen.  Tombstoned / empty tail entries count as +inf but keep their stored distance.
+__global__ void __launch_bounds__(kLinkWarps * 32)
+    reverse_apply_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist,
+                         const uint32_t* __restrict__ tomb, int R, int P, const uint32_t* __restrict__ ku,
+                         const uint64_t* __restrict__ kv, int64_t n, const uint32_t* __restrict__ heads,
+                         const unsigned int* __restrict__ nseg) {
+  __shared__ uint32_t old_id[kLinkWarps][128];
+  __shared__ float old_d[kLinkWarps][128];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned int S = *nseg;
+  const int TS = R - P;
+  for (unsigned int w = blockIdx.x * kLinkWarps + wib; w < S; w += gridDim.x * kLinkWarps) {
+    const int64_t start = heads[w];
+    const uint32_t u = ku[start];
+    if (tomb_dead(tomb, u)) continue;
+    int64_t end = start;
+    for (;;) {
+      const int64_t i = end + lane;
+      const unsigned same = __ballot_sync(0xffffffffu, i < n && ku[i] == u);
+      if (same == 0xffffffffu) {
+        end += 32;
+        continue;
+      }
+      end += __ffs(~same) - 1;
+      break;
+    }
+    uint64_t best[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = r * 32 + lane;
+      best[r] = kEmptyKey;
+      if (e < TS) {
+        const uint32_t id = graph[(size_t)u * R + P + e];
+        const float d = edge_dist[(size_t)u * R + P + e];
+        old_id[wib][e] = id;
+        old_d[wib][e] = d;
+        if (id != kSent) best[r] = make_key(tomb_dead(tomb, id) ? __int_as_float(0x7F800000) : d, id);
+      }
+    }
+    __syncwarp();
+    warp_sort<4>(best, lane);
+    for (int64_t c0 = start; c0 < end; c0 += 128) {
+      uint64_t cand[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t i = c0 + r * 32 + lane;
+        cand[r] = i < end ? kv[i] : kEmptyKey;
+      }
+      warp_sort<4>(cand, lane);
+      warp_merge_into<4, 4>(best, cand, lane);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = r * 32 + lane;
+      if (e < TS) {
+        const uint32_t id = key_id(best[r]);
+        float d = key_dist(best[r]);
+        if (id != kSent && __float_as_uint(d) == 0x7F800000u) {  // a tombstoned old entry: keep its distance
+          for (int s = 0; s < TS; ++s)
+            if (old_id[wib][s] == id) d = old_d[wib][s];
+        }
+        graph[(size_t)u * R + P + e] = id;
+        edge_dist[(size_t)u * R + P + e] = d;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int E>
+cudaError_t launch_detour_e(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
+                            const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
+  int mbits = 1;
+  while ((1 << mbits) < 2 * nc || (1 << mbits) < 256) ++mbits;  // >= 2x load factor, room for 128 tail keys
+  const int M = 1 << mbits;
+  const size_t per_warp = (((size_t)nc * 8 + (size_t)M * 6 + 16) + 15) & ~(size_t)15;
+  const size_t smem = per_warp * kLinkWarps;
+  auto kern = detour_select_kernel<E>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const unsigned blocks = (unsigned)((n_new + kLinkWarps - 1) / kLinkWarps);
+  kern<<<blocks, kLinkWarps * 32, smem, st>>>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, mbits);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_detour_select(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
+                                 const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
+  if (n_new <= 0) return cudaSuccess;
+  if (nc <= 32) return launch_detour_e<1>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
+  if (nc <= 64) return launch_detour_e<2>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
+  if (nc <= 128) return launch_detour_e<4>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
+  if (nc <= 256) return launch_detour_e<8>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
+  if (nc <= 512) return launch_detour_e<16>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
+  return cudaErrorInvalidValue;
+}
+
+static size_t cub_temp_bytes(int64_t m) {
+  size_t t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)m, 0, 32);
+  return t;
+}
+
+size_t reverse_scratch_bytes(int64_t n_new, int R) {
+  const int64_t m = n_new * R;
+  return (size_t)m * (4 + 4 + 8 + 8 + 4) + 256 + cub_temp_bytes(m) + 1024;
+}
+
+cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R, int P, int64_t first,
+                           int64_t n_new, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (n_new <= 0 || P >= R) return cudaSuccess;
+  const int64_t m = n_new * R;
+  auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  unsigned char* p = static_cast<unsigned char*>(scratch);
+  uint64_t* kv = reinterpret_cast<uint64_t*>(p);
+  p += align(m * 8);
+  uint64_t* kv2 = reinterpret_cast<uint64_t*>(p);
+  p += align(m * 8);
+  uint32_t* ku = reinterpret_cast<uint32_t*>(p);
+  p += align(m * 4);
+  uint32_t* ku2 = reinterpret_cast<uint32_t*>(p);
+  p += align(m * 4);
+  uint32_t* heads = reinterpret_cast<uint32_t*>(p);
+  p += align(m * 4);
+  unsigned int* nseg = reinterpret_cast<unsigned int*>(p);
+  p += 256;
+  size_t temp = cub_temp_bytes(m);
+  if ((size_t)(p - static_cast<unsigned char*>(scratch)) + temp > scratch_bytes) return cudaErrorInvalidValue;
+  const unsigned blocks = (unsigned)((m + 255) / 256);
+  reverse_emit_kernel<<<blocks, 256, 0, st>>>(graph, edge_dist, R, first, n_new, ku, kv);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(p, temp, ku, ku2, kv, kv2, (int)m, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(nseg, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  segment_heads_kernel<<<blocks, 256, 0, st>>>(ku2, m, heads, nseg);
+  const unsigned ablocks = (unsigned)std::min<int64_t>((m + kLinkWarps - 1) / kLinkWarps, 148 * 16);
+  reverse_apply_kernel<<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
+  return cudaGetLastError();
+}
+
+// ---- K-D: tombstones (lazy deletion) ------------------------------------------------------------------
+__global__ void tomb_check_kernel(const uint32_t* __restrict__ ids, int64_t n, uint64_t n_alloc, unsigned int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && (uint64_t)ids[i] >= n_alloc) *bad = 1u;
+}
+__global__ void tomb_set_kernel(const uint32_t* __restrict__ ids, int64_t n, uint32_t* tomb,
+                                unsigned long long* newly) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool fresh = false;
+  if (i < n) {
+    const uint32_t id = ids[i];
+    const uint32_t bit = 1u << (id & 31);
+    fresh = (atomicOr(tomb + (id >> 5), bit) & bit) == 0u;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, fresh);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(newly, (unsigned long long)__popc(m));
+}
+
+cudaError_t launch_tomb_check(const uint32_t* ids, int64_t n, uint64_t n_alloc, unsigned int* bad, cudaStream_t st) {
+  tomb_check_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, n, n_alloc, bad);
+  return cudaGetLastError();
+}
+cudaError_t launch_tomb_set(const uint32_t* ids, int64_t n, uint32_t* tomb, unsigned long long* newly,
+                            cudaStream_t st) {
+  tomb_set_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, n, tomb, newly);
+  return cudaGetLastError();
+}
+
+// ---- row helpers ---------------------------------------------------------------------------------------------------
+__global__ void pad_rows_kernel(const float* __restrict__ src, int64_t n, int dim, float* __restrict__ dst, int dp) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * dp) return;
+  const int64_t r = t / dp;
+  const int c = (int)(t - r * dp);
+  dst[t] = c < dim ? src[r * dim + c] : 0.f;
+}
+__global__ void unpad_rows_kernel(const float* __restrict__ src, int64_t n, int dp, float* __restrict__ dst, int dim) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * dim) return;
+  const int64_t r = t / dim;
+  dst[t] = src[r * dp + (t - r * dim)];
+}
+__global__ void fill_rows_kernel(uint32_t* graph, float* edge_dist, int64_t first, int64_t n, int R) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * R) return;
+  graph[first * R + t] = kSent;
+  edge_dist[first * R + t] = __int_as_float(0x7F800000);
+}
+
+cudaError_t launch_pad_rows(const float* src, int64_t n, int dim, float* dst, int dq, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t t = n * dq * 4;
+  pad_rows_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(src, n, dim, dst, dq * 4);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpad_rows(const float* src, int64_t n, int dq, float* dst, int dim, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t t = n * dim;
+  unpad_rows_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(src, n, dq * 4, dst, dim);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill_rows(uint32_t* graph, float* edge_dist, int64_t first, int64_t n, int R, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fill_rows_kernel<<<(unsigned)((n * R + 255) / 256), 256, 0, st>>>(graph, edge_dist, first, n, R);
+  return cudaGetLastError();
+}
+
+}  // namespace svf

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north star):
+  * integer-valued data: every fp32 distance is exact, so ids AND distances must be bit-exact, and so must the
+    search counters (iterations, expansions) and every adjacency / edge-distance update;
+  * float data: graph-search recall@10 within 0.005 of the oracle's on the same graph, exact-kNN ids bit-exact
+    except ties within 1e-5 relative distance, distances within 1e-4 relative;
+  * integer adjacency updates bit-exact given the same candidate sets.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import GLM, base_rows, int_rows, pack_tomb, query_rows, random_graph, random_tombstones
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+SENT = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def svf():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2601_08528_b200 import build_lib
+
+    build_lib.build()
+    import paper_2601_08528_b200 as m
+
+    return m
+
+
+def u32(t):
+    if isinstance(t, np.ndarray):
+        return t.view(np.uint32) if t.dtype == np.int32 else t
+    return t.cpu().numpy().view(np.uint32)
+
+
+def f32(t):
+    return t if isinstance(t, np.ndarray) else t.cpu().numpy()
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.fixture(scope="module")
+def c1():
+    """Config C1 (integer variant): 10K x 128 G-LM, R=32, 100 queries, graph by the oracle's build."""
+    X = base_rows("C1")
+    Q = query_rows("C1")
+    g, e = oracle.build(X, R=32)
+    return X, Q, g, e
+
+
+# ---- K-S search ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("L,p", [(16, 1), (32, 1), (64, 1), (128, 1), (256, 1), (48, 2), (100, 4), (512, 1)])
+def test_search_bit_exact_integer_data(svf, c1, L, p):
+    X, Q, g, e = c1
+    idx = svf.Index.from_state(X, g, e, search_width=p)
+    k = min(10, L)
+    ids, d = idx.search(cuda(Q), k, L)
+    cnt = idx.last_search_counters()
+    ri, rd, rc = oracle.graph_search(X, g, Q, k, L, p=p)
+    assert np.array_equal(u32(ids), ri)
+    assert np.array_equal(f32(d), rd)
+    assert cnt["iters"] == rc[:, 2].sum() and cnt["n_exp"] == rc[:, 1].sum()
+    assert cnt["n_dist"] >= rc[:, 0].sum()           # forgetting may recompute, never skip
+    assert cnt["n_dist"] <= 1.05 * rc[:, 0].sum()    # recompute ratio target
+
+
+@pytest.mark.parametrize("hash_bits", [7, 8, 9])
+def test_forgetful_visited_table_is_exact(svf, c1, hash_bits):
+    """Reading I7: clearing the table and re-registering the pool leaves results unchanged (tiny tables)."""
+    X, Q, g, e = c1
+    idx = svf.Index.from_state(X, g, e)
+    idx.set_search_params(1, 0, 0, hash_bits)
+    ids, d = idx.search(cuda(Q), 10, 32)
+    ri, rd, rc = oracle.graph_search(X, g, Q, 10, 32)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+    assert idx.last_search_counters()["n_dist"] > rc[:, 0].sum()  # the table really forgot
+
+
+def test_search_with_tombstones_and_caps(svf, c1):
+    X, Q, g, e = c1
+    dead = random_tombstones(len(X), 0.2, seed=7)
+    tomb = pack_tomb(dead, len(X))
+    idx = svf.Index.from_state(X, g, e, tomb=tomb)
+    assert idx.info()["n_deleted"] == len(dead)
+    ids, d = idx.search(cuda(Q), 10, 64)
+    ri, rd, _ = oracle.graph_search(X, g, Q, 10, 64, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+    assert not np.isin(u32(ids), dead).any()
+    idx.set_search_params(2, 40, 5, 0)
+    ids, d = idx.search(cuda(Q), 10, 64)
+    ri, rd, _ = oracle.graph_search(X, g, Q, 10, 64, p=2, n_init=40, max_iter=5, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+@pytest.mark.parametrize("dim,metric", [(128, 1), (96, 0), (200, 1), (13, 0), (3, 0)])
+def test_search_dims_and_metrics_integer(svf, dim, metric):
+    """Team sizes / padding (D not a multiple of 4) / inner product, ragged query count."""
+    X = int_rows(3000, dim, seed=dim, lo=-8 if metric else 0, hi=9 if metric else 64)
+    Q = int_rows(77, dim, seed=dim + 1, lo=-8 if metric else 0, hi=9 if metric else 64)
+    g = random_graph(3000, 24, seed=dim)
+    idx = svf.Index.from_state(X, g, metric=metric)
+    ids, d = idx.search(cuda(Q), 10, 64)
+    ri, rd, _ = oracle.graph_search(X, g, Q, 10, 64, metric=metric)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+def test_search_float_data_recall_parity(svf):
+    gen = GLM(dim=128, ell=32, s=1.0, m=0.0, sigma=0.05)
+    X = gen.rows(3, 3, 0, 20000)
+    Q = gen.rows(3, 4, 0, 300)
+    g, e = oracle.build(X, R=32, seed_size=2048, B_ins=2048, L_ins=64)
+    gt, gtd = oracle.bf_knn(X, Q, 10)
+    idx = svf.Index.from_state(X, g, e)
+    for L in (16, 32, 64):
+        ids, d = idx.search(cuda(Q), 10, L)
+        ri, rd, _ = oracle.graph_search(X, g, Q, 10, L)
+        r_gpu = oracle.recall_ids(u32(ids), gt, 10)
+        r_orc = oracle.recall_ids(ri, gt, 10)
+        assert abs(r_gpu - r_orc) <= 0.005, (L, r_gpu, r_orc)
+        same = (u32(ids) == ri)
+        assert same.mean() >= 0.99
+        np.testing.assert_allclose(f32(d)[same], rd[same], rtol=1e-5)
+
+
+def test_search_edge_cases(svf):
+    X = int_rows(40, 8, seed=1)
+    g = random_graph(40, 8, seed=2)
+    idx = svf.Index.from_state(X, g)
+    Q = int_rows(5, 8, seed=3)
+    # L >= N: equals exact kNN; k > live -> padding
+    ids, d = idx.search(cuda(Q), 10, 64)
+    gi, gd = oracle.bf_knn(X, Q, 10)
+    assert np.array_equal(u32(ids), gi) and np.array_equal(f32(d), gd)
+    idx.delete(np.arange(40, dtype=np.uint32))
+    ids, d = idx.search(cuda(Q), 10, 64)
+    assert np.all(u32(ids) == SENT) and np.all(np.isinf(f32(d)))
+    with pytest.raises(svf.SvfError):
+        idx.search(cuda(Q), 20, 10)        # k > itopk
+    with pytest.raises(svf.SvfError):
+        idx.search(cuda(Q), 10, 1024)      # itopk > 512
+    e_ids, e_d = idx.search(cuda(np.zeros((0, 8), np.float32)), 5, 16)
+    assert e_ids.shape == (0, 5)
+
+
+def test_host_pointer_path_matches_device_path(svf, c1):
+    X, Q, g, e = c1
+    idx = svf.Index.from_state(X, g, e)
+    ids_h, d_h = idx.search(Q, 10, 64)           # numpy in -> numpy out (staged through the ABI)
+    ids_d, d_d = idx.search(cuda(Q), 10, 64)
+    assert np.array_equal(u32(ids_h), u32(ids_d)) and np.array_equal(d_h, f32(d_d))
+
+
+# ---- K-G exact kNN / K-M merge ------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k,metric", [(1, 0), (10, 0), (33, 0), (100, 0), (10, 1), (250, 0)])
+def test_knn_exact_integer_bit_exact(svf, c1, k, metric):
+    X, Q, g, e = c1
+    if metric == 1:
+        X = X - 128.0
+        Q = Q - 128.0
+    dead = random_tombstones(len(X), 0.05, seed=3)
+    idx = svf.Index.from_state(X, g, metric=metric, tomb=pack_tomb(dead, len(X)))
+    ids, d = idx.knn_exact(cuda(Q), k)
+    ri, rd = oracle.bf_knn(X, Q, k, metric=metric, tomb=pack_tomb(dead, len(X)))
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+def test_knn_exact_float_tolerances(svf):
+    gen = GLM(dim=96, ell=24, s=1.0, m=0.0, sigma=0.05, normalize=True)
+    X = gen.rows(5, 5, 0, 30000)
+    Q = gen.rows(5, 6, 0, 200)
+    idx = svf.Index.from_state(X, random_graph(30000, 4, seed=1))
+    ids, d = idx.knn_exact(cuda(Q), 10)
+    ri, rd = oracle.bf_knn(X, Q, 10)
+    ids, d = u32(ids), f32(d)
+    np.testing.assert_allclose(d, rd, rtol=1e-4, atol=1e-6)
+    mism = ids != ri
+    # ids bit-exact except ties within 1e-5 relative distance
+    assert np.all(np.abs(d[mism] - rd[mism]) <= 1e-5 * np.abs(rd[mism]) + 1e-7)
+
+
+def test_merge_topk_matches_oracle(svf):
+    G, nq, k = 4, 300, 10
+    rng = np.random.default_rng(0)
+    ids = rng.integers(0, 10**6, size=(G, nq, k)).astype(np.uint32)
+    d = np.sort(rng.integers(0, 50, size=(G, nq, k)).astype(np.float32), axis=2)
+    ids[1, :5, 7:] = SENT
+    d[1, :5, 7:] = np.inf
+    mi, md = svf.merge_topk(cuda(ids.view(np.int32)), cuda(d))
+    ri, rd = oracle.merge_topk(ids, d)
+    assert np.array_equal(u32(mi), ri) and np.array_equal(f32(md), rd)
+
+
+# ---- K-L1 / K-L2 insert, K-D delete, build -------------------------------------------------------------------------
+@pytest.mark.parametrize("R,P,nc", [(32, 16, 64), (16, 8, 128), (24, 0, 48), (64, 32, 128), (8, 8, 30)])
+def test_link_candidates_bit_exact(svf, R, P, nc):
+    """Integer adjacency updates bit-exact given the same candidate sets (north star)."""
+    n0, nn = 4000, 700
+    gen = GLM(dim=24, ell=6, integer=True)
+    X = gen.rows(R, R, 0, n0 + nn)
+    g0, e0 = oracle.build(X[:n0], R=R, P=P, seed_size=800, B_ins=500, L_ins=max(nc, 32))
+    dead = random_tombstones(n0, 0.08, seed=R)
+    tomb = pack_tomb(dead, n0 + nn)
+    G = np.vstack([g0, np.full((nn, R), SENT, np.uint32)])
+    E = np.vstack([e0, np.full((nn, R), np.inf, np.float32)])
+    cid, cd, _ = oracle.graph_search(X, G, X[n0:], k=1, L=nc, tomb=tomb, n_alloc=n0, qidx=np.arange(n0, n0 + nn),
+                                     insert_mode=True)
+    gr, er = oracle.link_candidates(G, E, n0, cid, cd, P=P, tomb=tomb)
+    idx = svf.Index.from_state(X[:n0], g0, e0, tomb=pack_tomb(dead, n0), capacity=n0 + nn, protect_prefix=P)
+    idx.link_candidates(cid, cd, X=X[n0:])
+    st = idx.export()
+    assert np.array_equal(st["graph"], gr)
+    assert np.array_equal(st["edge_dist"], er)
+
+
+@pytest.mark.parametrize("B", [64, 333, 4096])
+def test_insert_bit_exact_integer_data(svf, c1, B):
+    X, Q, g, e = c1
+    n0 = 8000
+    g0, e0 = oracle.build(X[:n0], R=32)
+    dead = random_tombstones(n0, 0.05, seed=B)
+    tomb = pack_tomb(dead, len(X))
+    G = np.vstack([g0, np.full((len(X) - n0, 32), SENT, np.uint32)])
+    E = np.vstack([e0, np.full((len(X) - n0, 32), np.inf, np.float32)])
+    gr, er = oracle.insert(X, G, E, n_alloc=n0, n_new=len(X) - n0, P=16, B_ins=B, tomb=tomb)
+    idx = svf.Index.from_state(X[:n0], g0, e0, tomb=pack_tomb(dead, n0), capacity=len(X), insert_batch=B)
+    new_ids = idx.insert(cuda(X[n0:]))
+    assert np.array_equal(new_ids, np.arange(n0, len(X), dtype=np.uint32))
+    st = idx.export()
+    assert np.array_equal(st["graph"], gr)
+    assert np.array_equal(st["edge_dist"], er)
+    with pytest.raises(svf.SvfError) as ei:
+        idx.insert(cuda(X[:1]))                # capacity exhausted: nothing inserted
+    assert ei.value.status == 2 and idx.info()["n_alloc"] == len(X)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_build_bit_exact_integer_data(svf, metric):
+    gen = GLM(dim=32, ell=8, integer=True)
+    X = gen.rows(9, 9, 0, 6000) - (100.0 if metric else 0.0)
+    gr, er = oracle.build(X, R=24, seed_size=1000, B_ins=700, L_ins=64, metric=metric)
+    idx = svf.Index.build(cuda(X), degree=24, seed_size=1000, insert_batch=700, insert_itopk=64, metric=metric)
+    st = idx.export()
+    assert np.array_equal(st["graph"], gr)
+    assert np.array_equal(st["edge_dist"], er)
+    assert np.array_equal(st["vec"], X)
+
+
+def test_build_tiny_and_padding(svf):
+    X = np.array([[0.0], [1.0], [2.0], [3.0], [4.0]], np.float32)
+    idx = svf.Index.build(X, degree=2)
+    assert set(idx.export()["graph"][2].tolist()) == {1, 3}
+    X3 = int_rows(3, 4, seed=1)
+    idx = svf.Index.build(X3, degree=4)
+    g = idx.export()["graph"]
+    assert np.all((g != SENT).sum(1) == 2)
+
+
+def test_delete_semantics(svf, c1):
+    X, Q, g, e = c1
+    idx = svf.Index.from_state(X, g, e)
+    assert idx.delete(np.array([5, 6, 7], np.uint32)) == 3
+    assert idx.delete(np.array([5, 6, 8, 8], np.uint32)) == 1        # idempotent; duplicates counted once
+    with pytest.raises(svf.SvfError) as ei:
+        idx.delete(np.array([1, len(X)], np.uint32))                  # unknown id -> NOT_FOUND, nothing deleted
+    assert ei.value.status == 3 and idx.info()["n_deleted"] == 4
+    tomb = idx.export()["tomb"]
+    assert np.array_equal(tomb, pack_tomb([5, 6, 7, 8], len(X)))
+
+
+def test_read_after_write(svf, c1):
+    """insert x, then search x (k=1) returns x; paper Recall@1 0.96."""
+    X, Q, g, e = c1
+    n0 = 9000
+    idx = svf.Index.from_state(X[:n0], g[:n0] % n0, capacity=len(X), insert_batch=10)
+    idx.insert(cuda(X[n0:]))
+    ids, _ = idx.search(cuda(X[n0:]), 1, 32)
+    assert np.mean(u32(ids)[:, 0] == np.arange(n0, len(X))) >= 0.95
