@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the SVFusion hot path on B200.
+
+Default (N=1): BASELINE.json configs[1], SIFT1M-shaped C2: 1M x d128 fp32 (integer-valued G-LM), degree 64,
+10K-query batches, k=10, L2.  A *step* is one pass of the search hot path (S0-S8) over the 10K-query batch at the
+lowest itopk whose recall@10 (vs exact ground truth from svf_knn_exact) is >= 0.95.  Inserts/s and deletes/s
+(I0-I3, D1) are measured in the same run on 1% batches and reported beside the headline.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl svf|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (N>1: one 1M shard per rank, queries broadcast,
+                                                       NCCL all-gather of per-shard top-k + svf_merge_topk)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import base_rows, config_spec, query_rows  # noqa: E402
+
+L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 48, 64, 96, 128, 192, 256]
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="svf", choices=["svf", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--n", type=int, default=0, help="override rows per shard")
+    ap.add_argument("--nq", type=int, default=0, help="override query batch")
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--target-recall", type=float, default=0.95)
+    ap.add_argument("--itopk", type=int, default=0, help="fix itopk (skip the sweep)")
+    ap.add_argument("--search-width", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-insert", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="short run for ncu: no GT / sweep / baselines")
+    return ap.parse_args()
+
+
+# ---- distributed plumbing -------------------------------------------------------------------------------------
+class Dist:
+    def __init__(self, n_gpus: int):
+        import torch
+
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != n_gpus and self.world > 1:
+            raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.world}")
+        self.dev = torch.device("cuda", self.local)
+        torch.cuda.set_device(self.dev)
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampler around the timed region (the recipe's clocks line)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = subprocess.Popen(
+            ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,utilization.gpu", "--format=csv,noheader,nounits", "-lms", "100"],
+            stdout=self.f, stderr=subprocess.DEVNULL)
+
+    def stop(self) -> dict:
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 4]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        for r in rows:
+            try:
+                s, m, _, act, util = float(r[0]), float(r[1]), r[2], int(r[3].strip(), 16), float(r[4])
+            except ValueError:
+                continue
+            mx = max(mx, m)
+            if util > 0:
+                sm.append(s)
+            for bit, name in REASONS.items():
+                if act & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(sm)}
+
+
+def measured_peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic() -> dict | None:
+    """Per-query DRAM bytes of the search kernel from the committed ncu --set full summary (if any)."""
+    p = os.path.join(ROOT, "profiles", "ncu_search_latest.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def recall_at_k(ids: np.ndarray, gt: np.ndarray, k: int) -> float:
+    ids, gt = ids[:, :k], gt[:, :k]
+    hit = (ids[:, :, None] == gt[:, None, :]).any(axis=2).sum()
+    return float(hit) / (k * ids.shape[0])
+
+
+# ---- the GPU arm ----------------------------------------------------------------------------------------------------
+def run_svf(a):
+    import torch
+
+    import paper_2601_08528_b200 as svf
+
+    D = Dist(a.gpus)
+    c = config_spec(a.config)
+    n = a.n or c["n"]
+    nq = a.nq or c["nq"]
+    k, R, dim = a.k, c["degree"], c["dim"]
+    ins_batch = max(1, n // 100)                      # 1% insert / delete batches (C3-style rounds)
+    ins_steps = 10 if not a.no_insert else 0
+    ins_warm = 2 if not a.no_insert else 0
+    t0 = time.time()
+    X = base_rows(a.config, D.rank * n, n)            # shard r = global ids [r*n, (r+1)*n)
+    Q = query_rows(a.config, nq)                       # queries broadcast: every rank generates the same batch
+    Xnew = base_rows(a.config, D.world * n + D.rank * ins_batch * (ins_steps + ins_warm),
+                     ins_batch * (ins_steps + ins_warm)) if ins_steps else None
+    t_gen = time.time() - t0
+    dev = D.dev
+    Xd = torch.from_numpy(X).to(dev)
+    Qd = torch.from_numpy(Q).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    idx = svf.Index.build(Xd, degree=R, metric=c["metric"], capacity=n + (0 if Xnew is None else len(Xnew)),
+                          device=D.local, search_width=a.search_width)
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    del Xd
+    offset = D.rank * n
+
+    def gather_merge(ids, d):
+        """local top-k (local ids) -> global ids -> NCCL all-gather -> K-M merge (identical on every rank)."""
+        gids = (ids.to(torch.int64) + offset).to(torch.int32)
+        gids = torch.where(ids == -1, ids, gids)
+        if D.world == 1:
+            return gids, d
+        ai = torch.empty((D.world,) + tuple(gids.shape), dtype=gids.dtype, device=dev)
+        ad = torch.empty((D.world,) + tuple(d.shape), dtype=d.dtype, device=dev)
+        D.pg.all_gather_into_tensor(ai, gids)
+        D.pg.all_gather_into_tensor(ad, d)
+        return svf.merge_topk(ai, ad)
+
+    L = a.itopk
+    sweep, gt = [], None
+    if not a.ncu:
+        t0 = time.time()
+        gi, gd = idx.knn_exact(Qd, k)
+        gi, gd = gather_merge(gi, gd)
+        torch.cuda.synchronize()
+        t_gt = time.time() - t0
+        gt = gi.cpu().numpy()
+        for Ls in ([L] if L else L_SWEEP):
+            ids, d = gather_merge(*idx.search(Qd, k, Ls))
+            rec = recall_at_k(ids.cpu().numpy(), gt, k)
+            sweep.append({"itopk": Ls, "recall": round(rec, 4)})
+            if not L and rec >= a.target_recall:
+                L = Ls
+                break
+        if not L:
+            L = L_SWEEP[-1]
+    L = L or 16
+    recall = next((s["recall"] for s in sweep if s["itopk"] == L), None)
+
+    def step():
+        ids, d = idx.search(Qd, k, L)
+        if D.world > 1:
+            gather_merge(ids, d)
+
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+
+    def timed_region():
+        clocks = Clocks(dev.index or 0) if not a.ncu else None
+        for _ in range(a.warmup):
+            step()
+        idx.profile(True)
+        D.barrier()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()                       # ncu --profile-from-start off captures this range
+        for i in range(a.steps):
+            flush.zero_()                                 # L2 flush between timed iterations
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        D.barrier()
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+        prof = idx.profile_read()
+        idx.profile(False)
+        return ms, prof, (clocks.stop() if clocks else None)
+
+    ms_total, prof, clk = timed_region()
+    if clk and (BAD_REASONS & set(clk["reasons"])):      # rejected by the timing rules: re-measure once
+        ms_total, prof, clk = timed_region()
+        clk["remeasured"] = True
+    ms_total = D.max(ms_total)
+    ms_step = ms_total / a.steps
+    qps = nq / (ms_step / 1e3)
+    value = qps * D.world                                 # query-shard searches/s over all ranks
+    kern_ms, kern_n = prof["search"]
+    kern_avg_ms = kern_ms / max(kern_n, 1)
+    gpu_counters = idx.last_search_counters()
+
+    # ---- end to end through the public API: pinned host queries in, host results out ------------------------------
+    e2e = None
+    if not a.ncu:
+        Qh = torch.from_numpy(Q).pin_memory()
+        for _ in range(max(3, a.warmup // 4)):
+            idx.search(Qh, k, L)
+        D.barrier()
+        tt = []
+        for _ in range(max(10, a.steps // 4)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ids_h, d_h = idx.search(Qh, k, L)            # H2D + kernel + D2H + sync inside svf_search
+            tt.append(time.perf_counter() - t1)
+        e2e_s = D.max(float(np.mean(tt)))
+        e2e = {"value": round(nq * D.world / e2e_s, 1), "unit": "queries/s",
+               "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 8)}
+
+    # ---- CPU baseline: the oracle, as it stands, on the host cores, on the graph just timed (rank 0, N=1 only) ------
+    cpu, alg = None, None
+    if D.world == 1 and D.rank == 0 and not a.ncu and not a.no_cpu:
+        import oracle
+
+        cpu, cnt = cpu_baseline(oracle, idx.export(), Q, k, L, a.cpu_seconds)
+        alg = {"n_dist": float(cnt[:, 0].mean()), "n_exp": float(cnt[:, 1].mean()), "source": "oracle counters"}
+
+    # ---- inserts / deletes (I0-I3, D1) on 1% batches ---------------------------------------------------------------
+    ins = None
+    if ins_steps:
+        Xn = torch.from_numpy(Xnew).to(dev)
+        t_ins = []
+        idx.profile(True)
+        for j in range(ins_warm + ins_steps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            idx.insert(Xn[j * ins_batch:(j + 1) * ins_batch])
+            e1.record()
+            torch.cuda.synchronize()
+            if j >= ins_warm:
+                t_ins.append(e0.elapsed_time(e1))
+        iprof = idx.profile_read()
+        idx.profile(False)
+        rng = np.random.default_rng(1000 + D.rank)
+        live = idx.info()["n_alloc"]
+        t_del = []
+        for j in range(ins_steps):
+            ids_del = torch.from_numpy(rng.choice(live, ins_batch, replace=False).astype(np.int32)).to(dev)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            idx.delete(ids_del)
+            e1.record()
+            torch.cuda.synchronize()
+            t_del.append(e0.elapsed_time(e1))
+        ins_ms, del_ms = D.max(float(np.mean(t_ins))), D.max(float(np.mean(t_del)))
+        ins = {"inserts_per_s": round(ins_batch * D.world / (ins_ms / 1e3), 1),
+               "deletes_per_s": round(ins_batch * D.world / (del_ms / 1e3), 1),
+               "batch": ins_batch, "ms_per_insert_batch": round(ins_ms, 3), "ms_per_delete_batch": round(del_ms, 3),
+               "insert_breakdown_ms": {kk: round(v[0] / max(1, ins_warm + ins_steps), 3)
+                                       for kk, v in iprof.items() if kk != "search"},
+               "build_inserts_per_s": round(n / t_build, 1)}
+
+    if alg is None:
+        alg = {"n_dist": gpu_counters["n_dist"] / max(1, gpu_counters["queries"]),
+               "n_exp": gpu_counters["n_exp"] / max(1, gpu_counters["queries"]),
+               "source": "GPU counters (include visited-table recomputes)"}
+    bq = alg["n_dist"] * dim * 4 + alg["n_exp"] * R * 4 + dim * 4 + k * 8   # SURVEY §8(d) B_q
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = nq * bq / (kern_avg_ms / 1e3) / 1e9
+    tr = ncu_traffic()
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": (round(tr["dram_bytes_per_query"] * nq) if tr and tr.get("itopk") == L else None),
+            "kernel": "search_kernel", "kernel_avg_ms": round(kern_avg_ms, 4), "alg_bytes_per_query": round(bq, 1),
+            "alg_counts": alg, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst, measured)" if peaks else
+            "fallback 6650 GB/s (B200_PROFILING.md)"}
+
+    if D.rank == 0:
+        line = {
+            "metric": "QPS at recall@10>=0.95 (batch 10K) and inserts/sec",
+            "value": round(value, 1), "unit": "queries/s", "n_gpus": D.world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-LM, integer-valued; DESIGN.md)",
+            "config": {"workload": c["workload"], "n_per_gpu": n, "dim": dim, "degree": R, "batch": nq, "k": k,
+                       "itopk": L, "search_width": a.search_width, "recall_at_10": recall,
+                       "recall_sweep": sweep, "l2": "flushed between timed steps (256 MB write)",
+                       "parallelism": f"{D.world} shard(s), queries broadcast" +
+                                      (", NCCL all-gather + svf_merge_topk" if D.world > 1 else ""),
+                       "value_units": "queries x shards searched per second (== QPS at N=1)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "insert": ins, "clocks": clk,
+            "gpu_launches": a.steps * (1 if D.world == 1 else 2),
+            "setup_s": {"gen": round(t_gen, 2), "build": round(t_build, 2)},
+        }
+        print(json.dumps(line), flush=True)
+    idx.close()
+    D.close()
+
+
+def cpu_baseline(oracle, st, Q, k, L, seconds):
+    """Time oracle.graph_search (as it stands) on the exported graph with all host cores, bounded to ~seconds."""
+    threads = os.cpu_count() or 1
+    X, G = st["vec"], st["graph"]
+    tomb = st["tomb"] if st["tomb"].any() else None
+    probe = Q[:256]
+    t0 = time.perf_counter()
+    oracle.graph_search(X, G, probe, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+    per_q = (time.perf_counter() - t0) / len(probe)
+    nq_s = int(min(len(Q), max(256, seconds / max(per_q, 1e-9))))
+    sample = Q[:nq_s]
+    t0 = time.perf_counter()
+    _, _, cnt = oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+    dt = time.perf_counter() - t0
+    reps = 1
+    while dt * (reps + 1) / reps < seconds and reps < 50 and nq_s == len(Q):
+        t1 = time.perf_counter()
+        oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+        dt += time.perf_counter() - t1
+        reps += 1
+    return ({"value": round(nq_s * reps / dt, 1), "unit": "queries/s", "cores": threads, "kind": "oracle",
+             "sample": f"{nq_s} queries x {reps} pass(es) at itopk={L} on the exported GPU-built graph "
+                       f"(oracle graph_search_ref, std::thread x {threads})"}, cnt)
+
+
+# ---- the reference arm: the oracle, timed on the host cores ---------------------------------------------------------
+def run_reference(a):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    import torch
+
+    import oracle
+    import paper_2601_08528_b200 as svf
+
+    c = config_spec(a.config)
+    n = a.n or c["n"]
+    nq = a.nq or c["nq"]
+    k, R = a.k, c["degree"]
+    X = base_rows(a.config, 0, n)
+    Q = query_rows(a.config, nq)
+    # Input preparation (untimed): the graph is built by svf_build, which is bit-identical to oracle.build on this
+    # integer-valued workload (tests/test_gpu_parity.py::test_build_bit_exact_integer_data); exact ground truth by
+    # svf_knn_exact.  Only the oracle's search is timed.
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=R, metric=c["metric"])
+    gt, _ = idx.knn_exact(torch.from_numpy(Q).cuda(), k)
+    gt = gt.cpu().numpy()
+    st = idx.export()
+    idx.close()
+    threads = os.cpu_count() or 1
+    L = a.itopk
+    sweep = []
+    probe = Q[:1000]
+    for Ls in ([L] if L else L_SWEEP):
+        ids, _, _ = oracle.graph_search(st["vec"], st["graph"], probe, k, Ls, threads=threads)
+        rec = recall_at_k(ids.astype(np.int64).astype(np.int32), gt[:1000], k)
+        sweep.append({"itopk": Ls, "recall": round(rec, 4)})
+        if not L and rec >= a.target_recall:
+            L = Ls
+            break
+    L = L or L_SWEEP[-1]
+    t0 = time.perf_counter()
+    oracle.graph_search(st["vec"], st["graph"], Q[:256], k, L, threads=threads)
+    per_q = (time.perf_counter() - t0) / 256
+    budget = 150.0 / max(1, a.steps + a.warmup)
+    m = int(min(nq, max(64, budget / max(per_q, 1e-9))))
+    times = []
+    for i in range(a.warmup + a.steps):
+        s0 = (i * m) % nq
+        sample = np.roll(Q, -s0, axis=0)[:m]
+        t1 = time.perf_counter()
+        oracle.graph_search(st["vec"], st["graph"], sample, k, L, threads=threads)
+        if i >= a.warmup:
+            times.append(time.perf_counter() - t1)
+    ms = 1e3 * float(np.mean(times))
+    qps = m / (ms / 1e3)
+    line = {"impl": "reference", "metric": "QPS at recall@10>=0.95 (batch 10K) and inserts/sec",
+            "value": round(qps, 1), "unit": "queries/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64-accumulate (fp32 decisions)", "data": "synthetic (seeded G-LM, integer-valued)",
+            "config": {"workload": c["workload"], "n_per_gpu": n, "batch": nq, "k": k, "itopk": L,
+                       "recall_sweep_1000q": sweep, "step_sample_queries": m},
+            "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{m} queries per step at itopk={L}"},
+            "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_svf(args)

@@ -25,14 +25,22 @@ def _is_torch(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor)
 
 
+def _pinned(t) -> bool:
+    try:
+        return bool(t.is_pinned())
+    except Exception:
+        return False
+
+
 def _prep(x, np_dtype, torch_dtype):
-    """-> (pointer, keepalive, device or None)"""
+    """-> (pointer, keepalive, device or None or "pinned")"""
     if _is_torch(x):
         t = x.detach()
         if t.dtype != torch_dtype:
             t = t.to(torch_dtype)
         t = t.contiguous()
-        return t.data_ptr(), t, (t.device if t.is_cuda else None)
+        where = t.device if t.is_cuda else ("pinned" if _pinned(t) else None)
+        return t.data_ptr(), t, where
     a = np.ascontiguousarray(x, dtype=np_dtype)
     return a.ctypes.data, a, None
 
@@ -40,10 +48,15 @@ def _prep(x, np_dtype, torch_dtype):
 def _stream(device) -> Optional[int]:
     if device is None or torch is None:
         return None
+    if device == "pinned":
+        return torch.cuda.current_stream().cuda_stream
     return torch.cuda.current_stream(device).cuda_stream
 
 
 def _empty(shape, np_dtype, torch_dtype, device):
+    if device == "pinned":  # pinned host in -> pinned host out (the end-to-end path)
+        t = torch.empty(shape, dtype=torch_dtype, pin_memory=True)
+        return t.data_ptr(), t
     if device is not None:
         t = torch.empty(shape, dtype=torch_dtype, device=device)
         return t.data_ptr(), t
@@ -77,7 +90,7 @@ class Index:
         """Build(X_init): exact R-NN seed + batched-insert growth (svf_build)."""
         ptr, keep, dev = _prep(X, np.float32, torch.float32 if torch else None)
         n, dim = int(keep.shape[0]), int(keep.shape[1])
-        if dev is not None:
+        if dev is not None and dev != "pinned":
             kw.setdefault("device", dev.index or 0)
         p = default_params(dim, degree, capacity=capacity or n, **kw)
         h = ctypes.c_void_p()

@@ -119,7 +119,9 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.cpl = MP / 32;
   int minbits = 1;
   while ((1 << minbits) < 4 * std::max(LP, MP)) ++minbits;  // forgetful-table invariant (I7)
-  c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(11, minbits);
+  // default: >= ~2x the expected distinct visits (n_dist grows ~linearly in L)
+  const int autobits = L <= 24 ? 11 : (L <= 96 ? 12 : 13);
+  c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   if (c.hbits > 15) return why = "hash_bits too large", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
