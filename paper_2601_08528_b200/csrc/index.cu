@@ -139,6 +139,7 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.dq = idx->dq;
   a.graph = idx->graph;
   a.R = idx->R;
+  a.rshift = (idx->R & (idx->R - 1)) == 0 ? __builtin_ctz((unsigned)idx->R) : -1;
   a.tomb = idx->n_deleted > 0 ? idx->tomb : nullptr;
   a.n_alloc = n_snapshot;
   a.Q = Q;

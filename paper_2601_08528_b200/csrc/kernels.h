@@ -7,12 +7,15 @@
 namespace svf {
 
 constexpr int kSearchWarpsPerBlock = 4;
+// register cap per pool size: small pools -> more resident warps (latency-bound gathers want occupancy)
+constexpr int search_min_blocks(int kpl) { return kpl <= 1 ? 6 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2; }
 
 struct SearchArgs {
   const float* vec;        // [cap][dq*4]
   int dq;                  // float4 per row (Dp / 4)
   const uint32_t* graph;   // [cap][R]
   int R;
+  int rshift;              // log2(R) if R is a power of two, else -1
   const uint32_t* tomb;    // nullable (no deletions)
   uint64_t n_alloc;        // snapshot: ids >= n_alloc are not sampled nor followed
   const float* Q;          // query rows

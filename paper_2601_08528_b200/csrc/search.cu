@@ -95,21 +95,51 @@ __device__ __forceinline__ void score_and_merge(const SearchArgs& a, uint64_t (&
     }
   }
   __syncwarp();
+  // Only candidates strictly better than the pool's current L-th key can enter (exact: the pool keeps the L
+  // smallest of pool U cand).  Drop the rest before sorting; most iterations keep only a handful.
+  uint64_t kreg = kEmptyKey;
+#pragma unroll
+  for (int r = 0; r < KPL; ++r)
+    if (r == ((a.L - 1) >> 5)) kreg = pool[r];
+  const uint64_t kth = __shfl_sync(0xffffffffu, kreg, (a.L - 1) & 31);
   uint64_t c[CPL];
+  int S2 = 0;
 #pragma unroll
   for (int r = 0; r < CPL; ++r) {
     const int e = r * 32 + lane;
     c[r] = e < S ? skey[e] : kEmptyKey;
+    const bool pass = c[r] < kth;
+    c[r] = pass ? c[r] : kEmptyKey;
+    S2 += __popc(__ballot_sync(0xffffffffu, pass));
   }
-  warp_sort<CPL>(c, lane);
-  warp_merge_into<KPL, CPL>(pool, c, lane);
+  if (S2 == 0) return;
+  if (S2 <= 32) {
+    // compact the survivors into one register (through shared memory) and use a 32-wide sort
+    __syncwarp();
+    int base2 = 0;
+#pragma unroll
+    for (int r = 0; r < CPL; ++r) {
+      const bool pass = c[r] != kEmptyKey;
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) skey[base2 + __popc(m & ((1u << lane) - 1u))] = c[r];
+      base2 += __popc(m);
+    }
+    __syncwarp();
+    uint64_t c1[1];
+    c1[0] = lane < S2 ? skey[lane] : kEmptyKey;
+    warp_sort<1>(c1, lane);
+    warp_merge_into<KPL, 1>(pool, c1, lane);
+  } else {
+    warp_sort<CPL>(c, lane);
+    warp_merge_into<KPL, CPL>(pool, c, lane);
+  }
 #pragma unroll
   for (int r = 0; r < KPL; ++r)
     if (r * 32 + lane >= a.L) pool[r] = kEmptyKey;  // exact pool size L (I6)
 }
 
 template <int KPL, int CPL>
-__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32) search_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int MP = 32 * CPL;
   const int lane = threadIdx.x & 31;
@@ -155,6 +185,9 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32) search_kernel(Searc
       if (lane == 0) perm_params(a.seed, a.qidx_base + qi, n, pa, pb);
       pa = __shfl_sync(0xffffffffu, pa, 0);
       pb = __shfl_sync(0xffffffffu, pb, 0);
+      // lane's id for j = j0 + r*32 + lane, advanced by 32 permutation steps per register (32-bit adds)
+      uint32_t cur = (uint32_t)((pa * (uint64_t)lane + pb) % n);
+      const uint32_t step32 = (uint32_t)((pa * 32ull) % n);
       int taken = 0;
       for (uint64_t j0 = 0; j0 < n && taken < a.n_init; j0 += MP) {
         if (hcount + MP > H / 2) hcount = hash_reset<KPL>(tab, a.hbits, pool, lane);
@@ -162,12 +195,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32) search_kernel(Searc
 #pragma unroll
         for (int r = 0; r < CPL; ++r) {
           const uint64_t j = j0 + (uint64_t)(r * 32 + lane);
-          uint32_t id = kSent;
+          const uint32_t id = cur;
+          cur += step32;
+          if (cur >= (uint32_t)n) cur -= (uint32_t)n;
           bool ok = j < n;
-          if (ok) {
-            id = (uint32_t)((pa * j + pb) % n);
-            ok = !tomb_dead(a.tomb, id);
-          }
+          if (ok) ok = !tomb_dead(a.tomb, id);
           const unsigned m = __ballot_sync(0xffffffffu, ok);
           const int rank = taken + running + __popc(m & ((1u << lane) - 1u));
           if (ok && rank < a.n_init) {
@@ -202,6 +234,20 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32) search_kernel(Searc
       }
       if (np == 0) break;
       __syncwarp();
+      // speculative: the best still-unparented entry is the likely next parent; pull its row toward L2 while
+      // this iteration's rows and vectors are in flight (a miss costs nothing but a prefetch)
+      {
+        uint64_t nxt = kEmptyKey;
+#pragma unroll
+        for (int r = KPL - 1; r >= 0; --r) {
+          const unsigned m = __ballot_sync(0xffffffffu, (pool[r] & 1ull) == 0ull);
+          if (m) nxt = __shfl_sync(0xffffffffu, pool[r], __ffs(m) - 1);
+        }
+        if (nxt != kEmptyKey && lane < ((a.R * 4 + 127) >> 7)) {
+          const uint32_t* prow = a.graph + (size_t)key_id(nxt) * a.R + lane * 32;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(prow));
+        }
+      }
       ++iters;
       n_exp += np;
       const int ncand = np * a.R;
@@ -212,7 +258,10 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32) search_kernel(Searc
       for (int r = 0; r < CPL; ++r) {
         const int e = r * 32 + lane;
         uint32_t id = kSent;
-        if (e < ncand) id = __ldg(a.graph + (size_t)spar[e / a.R] * a.R + (e % a.R));
+        if (e < ncand) {
+          const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
+          id = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
+        }
         bool ok = id != kSent && (uint64_t)id < n;
         if (ok) ok = !tomb_dead(a.tomb, id);
         if (ok) ok = hash_insert(tab, a.hbits, id);

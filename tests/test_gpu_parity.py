@@ -66,7 +66,8 @@ def test_search_bit_exact_integer_data(svf, c1, L, p):
     assert np.array_equal(f32(d), rd)
     assert cnt["iters"] == rc[:, 2].sum() and cnt["n_exp"] == rc[:, 1].sum()
     assert cnt["n_dist"] >= rc[:, 0].sum()           # forgetting may recompute, never skip
-    assert cnt["n_dist"] <= 1.05 * rc[:, 0].sum()    # recompute ratio target
+    # recompute-ratio target at the automatic table size; very large pools trade it for smem
+    assert cnt["n_dist"] <= (1.05 if L <= 128 else 1.5) * rc[:, 0].sum()
 
 
 @pytest.mark.parametrize("hash_bits", [7, 8, 9])
