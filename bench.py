@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--itopk", type=int, default=0, help="fix itopk (skip the sweep)")
     ap.add_argument("--search-width", type=int, default=1)
+    ap.add_argument("--hash-bits", type=int, default=0, help="visited-table slots 2^b per query (0 = auto)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-insert", action="store_true")
@@ -175,6 +176,7 @@ def run_svf(a):
     torch.cuda.synchronize()
     t_build = time.time() - t0
     del Xd
+    idx.set_search_params(a.search_width, 0, 0, a.hash_bits)
     offset = D.rank * n
 
     def gather_merge(ids, d):

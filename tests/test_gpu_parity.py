@@ -58,6 +58,7 @@ def c1():
 def test_search_bit_exact_integer_data(svf, c1, L, p):
     X, Q, g, e = c1
     idx = svf.Index.from_state(X, g, e, search_width=p)
+    idx.set_search_params(p, 0, 0, 13 if L <= 128 else 0)   # a table >= 2x the visits: few recomputes
     k = min(10, L)
     ids, d = idx.search(cuda(Q), k, L)
     cnt = idx.last_search_counters()
