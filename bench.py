@@ -161,7 +161,7 @@ def run_svf(a):
     ins_steps = 10 if not a.no_insert else 0
     ins_warm = 2 if not a.no_insert else 0
     t0 = time.time()
-    X = base_rows(a.config, D.rank * n, n)            # shard r = global ids [r*n, (r+1)*n)
+    X = base_rows(a.config, D.rank * n, n)            # shard r: generator rows [r*n, (r+1)*n), global ids l*G+r
     Q = query_rows(a.config, nq)                       # queries broadcast: every rank generates the same batch
     Xnew = base_rows(a.config, D.world * n + D.rank * ins_batch * (ins_steps + ins_warm),
                      ins_batch * (ins_steps + ins_warm)) if ins_steps else None
@@ -177,31 +177,20 @@ def run_svf(a):
     t_build = time.time() - t0
     del Xd
     idx.set_search_params(a.search_width, 0, 0, a.hash_bits)
-    offset = D.rank * n
+    from paper_2601_08528_b200.sharded import ShardedIndex
 
-    def gather_merge(ids, d):
-        """local top-k (local ids) -> global ids -> NCCL all-gather -> K-M merge (identical on every rank)."""
-        gids = (ids.to(torch.int64) + offset).to(torch.int32)
-        gids = torch.where(ids == -1, ids, gids)
-        if D.world == 1:
-            return gids, d
-        ai = torch.empty((D.world,) + tuple(gids.shape), dtype=gids.dtype, device=dev)
-        ad = torch.empty((D.world,) + tuple(d.shape), dtype=d.dtype, device=dev)
-        D.pg.all_gather_into_tensor(ai, gids)
-        D.pg.all_gather_into_tensor(ad, d)
-        return svf.merge_topk(ai, ad)
+    sh = ShardedIndex(idx, D.rank, D.world)          # global id g = local * G + r
 
     L = a.itopk
     sweep, gt = [], None
     if not a.ncu:
         t0 = time.time()
-        gi, gd = idx.knn_exact(Qd, k)
-        gi, gd = gather_merge(gi, gd)
+        gi, gd = sh.knn_exact(Qd, k)
         torch.cuda.synchronize()
         t_gt = time.time() - t0
         gt = gi.cpu().numpy()
         for Ls in ([L] if L else L_SWEEP):
-            ids, d = gather_merge(*idx.search(Qd, k, Ls))
+            ids, d = sh.search(Qd, k, Ls)
             rec = recall_at_k(ids.cpu().numpy(), gt, k)
             sweep.append({"itopk": Ls, "recall": round(rec, 4)})
             if not L and rec >= a.target_recall:
@@ -213,9 +202,7 @@ def run_svf(a):
     recall = next((s["recall"] for s in sweep if s["itopk"] == L), None)
 
     def step():
-        ids, d = idx.search(Qd, k, L)
-        if D.world > 1:
-            gather_merge(ids, d)
+        sh.search(Qd, k, L)        # N=1: one svf_search; N>1: + NCCL all-gather + svf_merge_topk
 
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]

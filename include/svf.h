@@ -124,6 +124,14 @@ svf_status svf_import(const svf_params* p, const float* vec, const uint32_t* gra
 svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* cand_ids, const float* cand_d,
                                int64_t n_new, int32_t n_cand, void* stream);
 
+/* Exact-kNN engine: mode 0 = automatic (tcgen05 TF32 scoring + exact FFMA re-rank with a certificate, exact FFMA
+ * fallback for rejected queries; used when k <= 32 and query rows are 16-byte aligned), 1 = FFMA tiles only. */
+svf_status svf_set_knn_mode(svf_index* idx, int32_t mode);
+
+/* Exact-kNN counters since creation: out[0] = queries, out[1] = queries that took the FFMA fallback after the
+ * tensor-core certificate rejected them, out[2] = tensor-core launches. */
+svf_status svf_knn_stats(svf_index* idx, uint64_t out[3]);
+
 /* Search-time knobs (overrides the build params): search_width, n_init (0 = itopk), max_iter, hash_bits. */
 svf_status svf_set_search_params(svf_index* idx, int32_t search_width, int32_t n_init, int32_t max_iter,
                                  int32_t hash_bits);

@@ -176,6 +176,15 @@ class Index:
         check(lib().svf_last_search_counters(self._h, out))
         return {"n_dist": out[0], "iters": out[1], "n_exp": out[2], "queries": out[3]}
 
+    def set_knn_mode(self, mode: int):
+        """0 = tcgen05 TF32 scoring + exact re-rank (auto), 1 = FFMA tiles only."""
+        check(lib().svf_set_knn_mode(self._h, mode))
+
+    def knn_stats(self) -> dict:
+        out = (ctypes.c_uint64 * 3)()
+        check(lib().svf_knn_stats(self._h, out))
+        return {"queries": out[0], "fallbacks": out[1], "tc_calls": out[2]}
+
     def profile(self, enable: bool = True):
         check(lib().svf_profile(self._h, int(enable)))
 

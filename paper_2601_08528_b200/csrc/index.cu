@@ -29,6 +29,8 @@ struct svf_index {
   cudaStream_t last_stream = nullptr;
   bool poisoned = false;
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
+  int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
+  uint64_t knn_queries = 0, knn_fallbacks = 0, knn_tc_calls = 0;
   bool prof = false;
   double prof_ms[4] = {0, 0, 0, 0};
   int64_t prof_cnt[4] = {0, 0, 0, 0};
@@ -301,6 +303,25 @@ svf_status insert_present_rows(svf_index* idx, int64_t n, cudaStream_t st) {
   return SVF_OK;
 }
 
+// exact kNN over ids [0, n): tcgen05 TF32 path when supported, else the FFMA tile kernel
+cudaError_t run_knn(svf_index* idx, int64_t n, const uint32_t* tomb, const float* Q, int64_t q_stride, int q_dim,
+                    int64_t nq, int k, int64_t self_base, uint32_t* oi, float* od, cudaStream_t st) {
+  const bool tc = idx->knn_mode == 0 && knn_tc_supported(idx->dq, q_stride, Q, k);
+  const size_t need = tc ? knn_tc_scratch_bytes(nq, n, idx->dq, k) : knn_scratch_bytes(nq, k, std::max<int64_t>(n, 1));
+  cudaError_t e = ensure_scratch(idx, need, st);
+  if (e != cudaSuccess) return e;
+  idx->knn_queries += (uint64_t)nq;
+  if (!tc)
+    return launch_knn_exact(idx->vec, idx->dq, n, tomb, Q, q_stride, q_dim, nq, k, idx->p.metric, self_base, oi, od,
+                            idx->scratch, idx->scratch_bytes, idx->num_sms, st);
+  uint32_t fb = 0;
+  e = launch_knn_tc(idx->vec, idx->dq, n, tomb, Q, q_stride, q_dim, nq, k, idx->p.metric, self_base, oi, od,
+                    idx->scratch, idx->scratch_bytes, idx->num_sms, st, &fb);
+  idx->knn_fallbacks += fb;
+  idx->knn_tc_calls += 1;
+  return e;
+}
+
 svf_status enter(svf_index* idx) {
   if (!idx) return fail(SVF_ERR_INVALID, "index is NULL");
   if (idx->poisoned) return fail(SVF_ERR_POISONED, "index poisoned by an earlier CUDA failure");
@@ -348,11 +369,8 @@ svf_status svf_build(const svf_params* p, const float* X, int64_t n, void* strea
   if (put_rows(idx, X, 0, n, st) != cudaSuccess) return bail(cuda_fail(nullptr, cudaGetLastError(), "copy X"));
   // seed: exact R-NN of the first n0 rows (self excluded), written straight into the rows (prefix|tail layout)
   const int64_t n0 = std::min<int64_t>(n, idx->p.seed_size);
-  const size_t kb = knn_scratch_bytes(n0, idx->R, n0);
-  if (ensure_scratch(idx, kb, st) != cudaSuccess) return bail(cuda_fail(nullptr, cudaGetLastError(), "scratch"));
-  cudaError_t e = launch_knn_exact(idx->vec, idx->dq, n0, nullptr, idx->vec, idx->Dp, idx->Dp, n0, idx->R,
-                                   idx->p.metric, 0, idx->graph, idx->edge_dist, idx->scratch, idx->scratch_bytes,
-                                   idx->num_sms, st);
+  cudaError_t e = run_knn(idx, n0, nullptr, idx->vec, idx->Dp, idx->Dp, n0, idx->R, 0, idx->graph,
+                          idx->edge_dist, st);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "seed exact R-NN"));
   idx->n_alloc = n0;
   if (n > n0) {
@@ -523,9 +541,9 @@ svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, 
   const bool q_dev = is_device_ptr(Q), i_dev = is_device_ptr(out_ids), d_dev = is_device_ptr(out_dists);
   const size_t qb = q_dev ? 0 : al((size_t)nq * idx->D * 4);
   const size_t ob = al((size_t)nq * k * 4);
-  const size_t kb = al(knn_scratch_bytes(nq, k, std::max<int64_t>(idx->n_alloc, 1)));
-  CK(idx, ensure_scratch(idx, qb + 2 * ob + kb, st), "knn scratch");
-  char* sp = static_cast<char*>(idx->scratch);
+  // staging lives in its own buffer: the kNN kernels use the scratch arena
+  char* sp = nullptr;
+  if (qb + 2 * ob > 0) CK(idx, cudaMallocAsync(reinterpret_cast<void**>(&sp), qb + 2 * ob, st), "knn staging");
   const float* Qd = Q;
   if (!q_dev) {
     CK(idx, cudaMemcpyAsync(sp, Q, (size_t)nq * idx->D * 4, cudaMemcpyHostToDevice, st), "H2D queries");
@@ -534,12 +552,11 @@ svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, 
   uint32_t* oi = i_dev ? out_ids : reinterpret_cast<uint32_t*>(sp + qb);
   float* od = d_dev ? out_dists : reinterpret_cast<float*>(sp + qb + ob);
   CK(idx,
-     launch_knn_exact(idx->vec, idx->dq, idx->n_alloc, idx->n_deleted > 0 ? idx->tomb : nullptr, Qd, idx->D, idx->D,
-                      nq, k, idx->p.metric, -1, oi, od, sp + qb + 2 * ob, idx->scratch_bytes - qb - 2 * ob,
-                      idx->num_sms, st),
+     run_knn(idx, idx->n_alloc, idx->n_deleted > 0 ? idx->tomb : nullptr, Qd, idx->D, idx->D, nq, k, -1, oi, od, st),
      "knn kernel");
   if (!i_dev) CK(idx, cudaMemcpyAsync(out_ids, oi, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
   if (!d_dev) CK(idx, cudaMemcpyAsync(out_dists, od, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
+  if (sp) CK(idx, cudaFreeAsync(sp, st), "knn staging free");
   if (!i_dev || !d_dev) CK(idx, cudaStreamSynchronize(st), "knn sync");
   return SVF_OK;
 }
@@ -646,6 +663,25 @@ svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
     out[1] += h[q * 3 + 1];
     out[2] += h[q * 3 + 2];
   }
+  return SVF_OK;
+}
+
+svf_status svf_set_knn_mode(svf_index* idx, int32_t mode) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (mode < 0 || mode > 1) return fail(SVF_ERR_INVALID, "knn mode must be 0 (auto) or 1 (FFMA)");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->knn_mode = mode;
+  return SVF_OK;
+}
+
+svf_status svf_knn_stats(svf_index* idx, uint64_t out[3]) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  out[0] = idx->knn_queries;
+  out[1] = idx->knn_fallbacks;
+  out[2] = idx->knn_tc_calls;
   return SVF_OK;
 }
 

@@ -59,6 +59,14 @@ cudaError_t launch_knn_exact(const float* vec, int dq, int64_t n, const uint32_t
                              uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
                              cudaStream_t st);
 
+// K-G on tcgen05 (TF32) + K-R exact re-rank + certificate + exact FFMA fallback (knn_tc.cu)
+bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k);
+size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k);
+cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
+                          int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
+                          uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
+                          cudaStream_t st, uint32_t* n_fallback);
+
 // K-M: merge G lists [G][nq][k] (ids/dists) -> first k per query by (dist, id)
 cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
                               float* out_d, cudaStream_t st);

@@ -1,0 +1,546 @@
+// K-G on the 5th-generation tensor cores: exact k-NN ("ground truth via exhaustive linear scan", P:L695;
+// SURVEY §8(a) G1) as a TF32 tcgen05 GEMM with a fused approximate top-k epilogue, followed by K-R, an exact
+// fp32 re-rank with a certificate, and an exact FFMA fallback for the (rare) queries the certificate rejects.
+//
+// knn_tc_kernel (persistent, one CTA per SM, 192 threads):
+//   warp 0      TMA producer: the 128-query A tile once per unit (K-major, SWIZZLE_128B, Dp/32 boxes of 128x32),
+//               then 256-row x 32-float B boxes of the base vectors through an S-stage mbarrier ring;
+//   warp 1      TMEM owner (512 columns = 2 accumulators of 128 lanes x 256 fp32) and single-thread MMA issuer:
+//               4 x tcgen05.mma.kind::tf32 (M=128, N=256, K=8) per 32-float chunk; tcgen05.commit frees the stage
+//               and, after the last chunk, publishes the accumulator;
+//   warps 2..5  epilogue: thread = query row = TMEM lane; tcgen05.ld 32 columns at a time, approximate score
+//               s~ = ||x||^2 - 2 q.x (L2) or -q.x (IP), keep the 32 smallest per (query, split) in registers.
+// knn_rerank_kernel (warp per query): merge the per-split lists to the best 64 approximate candidates, recompute
+//   their distances exactly (direct-difference FFMA, the search kernel's arithmetic), sort, emit the top k, and
+//   check the certificate  d_k < tau - E + ||q||^2  (tau = smallest score any excluded row can have, E = the
+//   TF32 error bound; E = 0 when data and query are integers <= 2047 whose sums fit 2^24, as in C1/C2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svf {
+
+namespace {
+
+constexpr int TC_M = 128, TC_N = 256, TC_KC = 32, TC_LIST = 32;
+constexpr int kTcThreads = 192;
+constexpr uint32_t kBStageBytes = TC_N * TC_KC * 4;  // 32 KB
+constexpr uint32_t kAChunkBytes = TC_M * TC_KC * 4;  // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// K-major operand, SWIZZLE_128B canonical layout: 128-byte rows, 8-row (1024 B) swizzle atoms, SBO = 1024 B
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address  [0,14)
+  d |= (uint64_t)1 << 16;                    // LBO = 16 B      [16,30)  (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO = 1024 B    [32,46)
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                    // layout type: SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                            ((uint32_t)(TC_M >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcArgs {
+  int64_t nq, n;         // queries, base rows (ids [0, n))
+  int kc;                // 32-float K chunks (Dp / 32 rounded up)
+  int stages;            // B ring depth
+  int64_t rows_per_split;
+  int64_t splits, units; // units = qtiles * splits
+  const float* norms;    // ||x||^2 per row (L2); unused for IP
+  const uint32_t* tomb;
+  int64_t self_base;     // >= 0: exclude id == self_base + query
+  int metric;
+  uint64_t* cand;        // [splits][nq][TC_LIST] keys (approx score, id), sorted ascending
+};
+
+template <bool kTomb, bool kSelf>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    knn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap xmap, TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned operand area (SWIZZLE_128B atoms)
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;                                   // kc x 16 KB
+  unsigned char* sB = sA + (size_t)a.kc * kAChunkBytes;       // stages x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)a.stages * kBStageBytes);
+  uint64_t* full = bars;                   // [stages]
+  uint64_t* empty = full + a.stages;       // [stages]
+  uint64_t* a_full = empty + a.stages;     // [1]
+  uint64_t* a_empty = a_full + 1;          // [1]
+  uint64_t* t_full = a_empty + 1;          // [2]
+  uint64_t* t_empty = t_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(t_full + i, 1);
+      mbar_init(t_empty + i, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t qtiles = (a.nq + TC_M - 1) / TC_M;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      uint32_t stage = 0, phase = 0, aphase = 0;
+      for (int64_t u = blockIdx.x; u < a.units; u += gridDim.x) {
+        const int64_t qt = u % qtiles, sp = u / qtiles;
+        const int64_t r0 = sp * a.rows_per_split, r1 = min(a.n, r0 + a.rows_per_split);
+        mbar_wait(a_empty, aphase ^ 1);
+        aphase ^= 1;
+        mbar_expect_tx(a_full, (uint32_t)a.kc * kAChunkBytes);
+        for (int c = 0; c < a.kc; ++c)
+          tma_load_2d(sA + (size_t)c * kAChunkBytes, &qmap, a_full, c * TC_KC, (int)(qt * TC_M));
+        for (int64_t nb = r0; nb < r1; nb += TC_N) {
+          for (int c = 0; c < a.kc; ++c) {
+            mbar_wait(empty + stage, phase ^ 1);
+            mbar_expect_tx(full + stage, kBStageBytes);
+            tma_load_2d(sB + (size_t)stage * kBStageBytes, &xmap, full + stage, c * TC_KC, (int)nb);
+            if (++stage == (uint32_t)a.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      uint32_t stage = 0, phase = 0, aphase = 0, acc = 0, tphase[2] = {0, 0};
+      for (int64_t u = blockIdx.x; u < a.units; u += gridDim.x) {
+        const int64_t sp = u / qtiles;
+        const int64_t r0 = sp * a.rows_per_split, r1 = min(a.n, r0 + a.rows_per_split);
+        mbar_wait(a_full, aphase);
+        aphase ^= 1;
+        for (int64_t nb = r0; nb < r1; nb += TC_N) {
+          mbar_wait(t_empty + acc, tphase[acc] ^ 1);
+          tphase[acc] ^= 1;
+          tc_fence_after();
+          const uint32_t d = tmem_base + acc * TC_N;
+          for (int c = 0; c < a.kc; ++c) {
+            mbar_wait(full + stage, phase);
+            tc_fence_after();
+            const uint32_t abase = smem_u32(sA + (size_t)c * kAChunkBytes);
+            const uint32_t bbase = smem_u32(sB + (size_t)stage * kBStageBytes);
+#pragma unroll
+            for (int kk = 0; kk < TC_KC / 8; ++kk)  // K = 8 tf32 (32 bytes) per MMA
+              umma_tf32(d, sdesc(abase + kk * 32), sdesc(bbase + kk * 32), (c | kk) ? 1u : 0u);
+            umma_commit(empty + stage);
+            if (++stage == (uint32_t)a.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(t_full + acc);
+          acc ^= 1;
+        }
+        umma_commit(a_empty);  // the A tile may be replaced once every MMA of this unit is done
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2..5, thread = query row = TMEM lane ----------------
+    const int lq = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = lq * 32 + lane;
+    uint32_t acc = 0, tphase[2] = {0, 0};
+    for (int64_t u = blockIdx.x; u < a.units; u += gridDim.x) {
+      const int64_t qt = u % qtiles, sp = u / qtiles;
+      const int64_t r0 = sp * a.rows_per_split, r1 = min(a.n, r0 + a.rows_per_split);
+      const int64_t qi = qt * TC_M + row;
+      float bv[TC_LIST];
+      uint32_t bi[TC_LIST];
+#pragma unroll
+      for (int i = 0; i < TC_LIST; ++i) {
+        bv[i] = __int_as_float(0x7F800000);
+        bi[i] = kSent;
+      }
+      for (int64_t nb = r0; nb < r1; nb += TC_N) {
+        mbar_wait(t_full + acc, tphase[acc]);
+        tphase[acc] ^= 1;
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * TC_N;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TC_N; c0 += 32) {
+          uint32_t v[32];
+          __syncwarp();
+          tmem_ld32(taddr + c0, v);
+          const int64_t cb = nb + c0;
+          const float nrm = (a.metric == 0 && cb + lane < r1) ? __ldg(a.norms + cb + lane) : 0.f;
+          uint32_t dead = 0;
+          if (kTomb && cb < r1) dead = __ldg(a.tomb + (cb >> 5));
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float nj = __shfl_sync(0xffffffffu, nrm, j);
+            const float dot = __uint_as_float(v[j]);
+            const float s = a.metric == 0 ? fmaf(-2.f, dot, nj) : -dot;
+            bool ok = (cb + j < r1) && s < bv[TC_LIST - 1];
+            if (kTomb) ok = ok && !((dead >> j) & 1u);
+            if (kSelf) ok = ok && (cb + j != a.self_base + qi);
+            if (ok) {  // insert (s, id) into the ascending register list, dropping the largest
+              const uint32_t id = (uint32_t)(cb + j);
+#pragma unroll
+              for (int i = TC_LIST - 1; i > 0; --i) {
+                const bool shift = bv[i - 1] > s;
+                const bool here = !shift && bv[i] > s;
+                bv[i] = shift ? bv[i - 1] : (here ? s : bv[i]);
+                bi[i] = shift ? bi[i - 1] : (here ? id : bi[i]);
+              }
+              if (bv[0] > s) {
+                bv[0] = s;
+                bi[0] = id;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(t_empty + acc);
+        acc ^= 1;
+      }
+      if (qi < a.nq) {
+        uint64_t* dst = a.cand + ((size_t)sp * a.nq + qi) * TC_LIST;
+#pragma unroll
+        for (int i = 0; i < TC_LIST; ++i) dst[i] = bi[i] == kSent ? kEmptyKey : make_key(bv[i], bi[i]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ||x||^2 per row (fp32 FFMA) + dataset facts for the TF32 error bound: max ||x||, all values integer <= 2047
+__global__ void row_norms_kernel(const float* __restrict__ vec, int dp, int64_t n, float* __restrict__ norms,
+                                 unsigned int* __restrict__ facts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  float acc = 0.f;
+  bool integral = true;
+  for (int c = lane; c < dp; c += 32) {
+    const float x = __ldg(vec + r * dp + c);
+    acc = fmaf(x, x, acc);
+    integral = integral && (x == rintf(x)) && fabsf(x) <= 2047.f;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  const bool all_int = __all_sync(0xffffffffu, integral);
+  if (lane == 0) {
+    norms[r] = acc;
+    atomicMax(facts + 0, __float_as_uint(sqrtf(acc)));  // positive floats order like their bit patterns
+    if (!all_int) atomicAnd(facts + 1, 0u);
+  }
+}
+
+// K-R: exact re-rank of the approximate candidates + certificate (warp per query)
+__global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t splits, int64_t nq, int k,
+                                  const float* __restrict__ vec, int dq, const float* __restrict__ Q,
+                                  int64_t q_stride, int q_dim, int metric, const unsigned int* __restrict__ facts,
+                                  uint32_t* __restrict__ out_ids, float* __restrict__ out_d,
+                                  uint32_t* __restrict__ fail_list, unsigned int* __restrict__ n_fail) {
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (qi >= nq) return;
+  // merge the per-split approximate lists into the best 64; tau = least score an excluded row can have
+  uint64_t best[2] = {kEmptyKey, kEmptyKey};
+  float tau = __int_as_float(0x7F800000);
+  for (int64_t s = 0; s < splits; ++s) {
+    uint64_t c[1];
+    c[0] = cand[((size_t)s * nq + qi) * TC_LIST + lane];
+    const uint64_t last = __shfl_sync(0xffffffffu, c[0], 31);
+    if (last != kEmptyKey) tau = fminf(tau, key_dist(last));  // a full list excluded rows scoring >= its max
+    warp_merge_into<2, 1>(best, c, lane);
+  }
+  const uint64_t m64 = __shfl_sync(0xffffffffu, best[1], 31);
+  if (m64 != kEmptyKey) tau = fminf(tau, key_dist(m64));
+  // exact distances of the (up to) 64 candidates: lane handles 2, full row each (rows are L2/HBM gathers)
+  const float* q = Q + (size_t)qi * q_stride;
+  float qn = 0.f;
+  for (int c = lane; c < q_dim; c += 32) qn = fmaf(q[c], q[c], qn);
+  bool qint = true;
+  for (int c = lane; c < q_dim; c += 32) qint = qint && (q[c] == rintf(q[c])) && fabsf(q[c]) <= 2047.f;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) qn += __shfl_xor_sync(0xffffffffu, qn, off);
+  qint = __all_sync(0xffffffffu, qint);
+  uint64_t ex[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint32_t id = key_id(best[r]);
+    ex[r] = kEmptyKey;
+    if (id != kSent) {
+      const float4* x4 = reinterpret_cast<const float4*>(vec + (size_t)id * dq * 4);
+      float acc = 0.f;
+      for (int c4 = 0; c4 < dq; ++c4) {
+        const float4 x = __ldg(x4 + c4);
+        const int c = c4 * 4;
+        const float q0 = c < q_dim ? q[c] : 0.f, q1 = c + 1 < q_dim ? q[c + 1] : 0.f;
+        const float q2 = c + 2 < q_dim ? q[c + 2] : 0.f, q3 = c + 3 < q_dim ? q[c + 3] : 0.f;
+        if (metric == 0) {
+          float d0 = x.x - q0, d1 = x.y - q1, d2 = x.z - q2, d3 = x.w - q3;
+          acc = fmaf(d0, d0, acc);
+          acc = fmaf(d1, d1, acc);
+          acc = fmaf(d2, d2, acc);
+          acc = fmaf(d3, d3, acc);
+        } else {
+          acc = fmaf(x.x, q0, acc);
+          acc = fmaf(x.y, q1, acc);
+          acc = fmaf(x.z, q2, acc);
+          acc = fmaf(x.w, q3, acc);
+        }
+      }
+      ex[r] = make_key((metric == 0 ? acc : -acc) + 0.0f, id);
+    }
+  }
+  warp_sort<2>(ex, lane);
+  if (lane < k) {
+    out_ids[qi * k + lane] = key_id(ex[0]);
+    out_d[qi * k + lane] = key_dist(ex[0]);
+  }
+  if (k > 32 && lane + 32 < k) {
+    out_ids[qi * k + 32 + lane] = key_id(ex[1]);
+    out_d[qi * k + 32 + lane] = key_dist(ex[1]);
+  }
+  // certificate: every excluded row has true score >= tau - E; accept if the exact k-th beats that strictly
+  const uint64_t kk = __shfl_sync(0xffffffffu, k <= 32 ? ex[0] : ex[1], (k - 1) & 31);
+  if (lane == 0 && tau != __int_as_float(0x7F800000)) {
+    const double xmax = (double)__uint_as_float(facts[0]);
+    const double qnorm = sqrt((double)qn);
+    const int D = dq * 4;
+    const bool exact = facts[1] != 0u && qint && qnorm * xmax < 8388608.0 && xmax * xmax < 16777216.0;
+    double E = 0.0;
+    if (!exact) {
+      const double u = 1.0 / 512.0 + (D + 9) * 2.384185791015625e-07;  // 2^-9 + (D+9) 2^-22
+      E = (metric == 0 ? 2.0 : 1.0) * u * qnorm * xmax + (D + 1) * 5.9604644775390625e-08 * (xmax * xmax + qn) +
+          1e-30;
+    }
+    const double dk = (double)key_dist(kk) * (exact ? 1.0 : 1.0 + (D + 2) * 5.9604644775390625e-08);
+    const double bound = (double)tau - E + (metric == 0 ? (double)qn : 0.0);
+    if (kk == kEmptyKey || !(dk < bound)) fail_list[atomicAdd(n_fail, 1u)] = (uint32_t)qi;
+  }
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ Q, int64_t q_stride, int q_dim,
+                                   const uint32_t* __restrict__ rows, int64_t m, float* __restrict__ dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * q_dim) return;
+  const int64_t r = t / q_dim;
+  dst[t] = Q[(size_t)rows[r] * q_stride + (t - r * q_dim)];
+}
+__global__ void scatter_results_kernel(const uint32_t* __restrict__ rows, int64_t m, int k,
+                                       const uint32_t* __restrict__ src_ids, const float* __restrict__ src_d,
+                                       uint32_t* __restrict__ out_ids, float* __restrict__ out_d) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * k) return;
+  const int64_t r = t / k;
+  out_ids[(size_t)rows[r] * k + (t - r * k)] = src_ids[t];
+  out_d[(size_t)rows[r] * k + (t - r * k)] = src_d[t];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {TC_KC, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TcPlan {
+  int kc, stages;
+  int64_t splits, rows_per_split, units, qtiles;
+  size_t smem;
+};
+TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
+  TcPlan p;
+  p.kc = (dq * 4 + TC_KC - 1) / TC_KC;
+  const size_t a_bytes = (size_t)p.kc * kAChunkBytes;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  p.stages = (int)std::min<size_t>(6, (budget - a_bytes) / kBStageBytes);
+  p.qtiles = (nq + TC_M - 1) / TC_M;
+  const int64_t ntiles = std::max<int64_t>(1, (n + TC_N - 1) / TC_N);
+  int64_t s = std::max<int64_t>(1, (8LL * num_sms + p.qtiles - 1) / p.qtiles);  // ~8 units per SM
+  s = std::min(s, ntiles);
+  p.rows_per_split = (ntiles + s - 1) / s * TC_N;
+  p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
+  if (p.splits < 1) p.splits = 1;
+  p.units = p.qtiles * p.splits;
+  p.smem = 1024 + a_bytes + (size_t)p.stages * kBStageBytes + 256;
+  return p;
+}
+
+}  // namespace
+
+bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k) {
+  const int kc = (dq * 4 + TC_KC - 1) / TC_KC;
+  return k <= 32 && (q_stride * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0 &&
+         (size_t)kc * kAChunkBytes + 2 * kBStageBytes + 2048 <= 227 * 1024 && get_encode() != nullptr;
+}
+
+size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
+  TcPlan p = tc_plan(nq, n, dq, 148);
+  TcPlan p2 = tc_plan(nq, n, dq, 512);
+  const int64_t s = std::max(p.splits, p2.splits);
+  // cand + norms + facts + fail list + fallback buffers (rows, ids, dists) + FFMA fallback scratch
+  return (size_t)s * nq * TC_LIST * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
+         (size_t)nq * k * 8 + knn_scratch_bytes(nq, k, n) + 8 * 256;
+}
+
+cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
+                          int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
+                          uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
+                          cudaStream_t st, uint32_t* n_fallback) {
+  if (nq <= 0) return cudaSuccess;
+  TcPlan p = tc_plan(nq, n, dq, num_sms);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  unsigned char* sp = static_cast<unsigned char*>(scratch);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(sp);
+  sp += al((size_t)p.splits * nq * TC_LIST * 8);
+  float* norms = reinterpret_cast<float*>(sp);
+  sp += al((size_t)n * 4);
+  unsigned int* facts = reinterpret_cast<unsigned int*>(sp);  // [0] max norm bits, [1] integral, [2] n_fail
+  sp += 256;
+  uint32_t* fail_list = reinterpret_cast<uint32_t*>(sp);
+  sp += al((size_t)nq * 4);
+  float* fbQ = reinterpret_cast<float*>(sp);
+  sp += al((size_t)nq * q_dim * 4);
+  uint32_t* fb_ids = reinterpret_cast<uint32_t*>(sp);
+  sp += al((size_t)nq * k * 4);
+  float* fb_d = reinterpret_cast<float*>(sp);
+  sp += al((size_t)nq * k * 4);
+  if ((size_t)(sp - static_cast<unsigned char*>(scratch)) > scratch_bytes) return cudaErrorInvalidValue;
+  const size_t rest = scratch_bytes - (size_t)(sp - static_cast<unsigned char*>(scratch));
+
+  CUtensorMap qmap, xmap;
+  if (!make_map(&qmap, Q, (uint64_t)q_dim, (uint64_t)nq, (uint64_t)q_stride * 4, TC_M) ||
+      !make_map(&xmap, vec, (uint64_t)dq * 4, (uint64_t)n, (uint64_t)dq * 16, TC_N))
+    return cudaErrorInvalidValue;
+  unsigned int init[3] = {0u, 1u, 0u};
+  cudaError_t e = cudaMemcpyAsync(facts, init, sizeof init, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  row_norms_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(vec, dq * 4, n, norms, facts);
+  TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, norms, tomb, self_base, metric, cand};
+  auto launch = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e2 != cudaSuccess) return e2;
+    const unsigned grid = (unsigned)std::min<int64_t>(p.units, num_sms);
+    kern<<<grid, kTcThreads, p.smem, st>>>(qmap, xmap, a);
+    return cudaGetLastError();
+  };
+  if (tomb && self_base >= 0) e = launch(knn_tc_kernel<true, true>);
+  else if (tomb) e = launch(knn_tc_kernel<true, false>);
+  else if (self_base >= 0) e = launch(knn_tc_kernel<false, true>);
+  else e = launch(knn_tc_kernel<false, false>);
+  if (e != cudaSuccess) return e;
+  knn_rerank_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits, nq, k, vec, dq, Q, q_stride, q_dim,
+                                                               metric, facts, out_ids, out_d, fail_list, facts + 2);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // exact FFMA fallback for the queries the certificate rejected
+  unsigned int hf = 0;
+  if ((e = cudaMemcpyAsync(&hf, facts + 2, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (n_fallback) *n_fallback = hf;
+  if (hf > 0) {
+    if (self_base >= 0)  // seed build on non-integral data: redo the (small) seed exactly with FFMA
+      return launch_knn_exact(vec, dq, n, tomb, Q, q_stride, q_dim, nq, k, metric, self_base, out_ids, out_d, sp,
+                              rest, num_sms, st);
+    gather_rows_kernel<<<(unsigned)((hf * (int64_t)q_dim + 255) / 256), 256, 0, st>>>(Q, q_stride, q_dim, fail_list,
+                                                                                       hf, fbQ);
+    e = launch_knn_exact(vec, dq, n, tomb, fbQ, q_dim, q_dim, hf, k, metric, -1, fb_ids, fb_d, sp, rest, num_sms, st);
+    if (e != cudaSuccess) return e;
+    scatter_results_kernel<<<(unsigned)((hf * (int64_t)k + 255) / 256), 256, 0, st>>>(fail_list, hf, k, fb_ids, fb_d,
+                                                                                      out_ids, out_d);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace svf
