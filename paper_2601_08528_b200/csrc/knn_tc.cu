@@ -27,7 +27,8 @@ namespace svf {
 namespace {
 
 constexpr int TC_M = 128, TC_N = 256, TC_KC = 32, TC_LIST = 32;
-constexpr int kTcThreads = 192;
+constexpr int kTcEpiWarps = 8;                       // 2 per TMEM lane quarter, 128 columns each
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr uint32_t kBStageBytes = TC_N * TC_KC * 4;  // 32 KB
 constexpr uint32_t kAChunkBytes = TC_M * TC_KC * 4;  // 16 KB
 
@@ -108,7 +109,7 @@ struct TcArgs {
   const uint32_t* tomb;
   int64_t self_base;     // >= 0: exclude id == self_base + query
   int metric;
-  uint64_t* cand;        // [splits][nq][TC_LIST] keys (approx score, id), sorted ascending
+  uint64_t* cand;        // [splits*2][nq][TC_LIST] keys (approx score, id), sorted ascending
 };
 
 template <bool kTomb, bool kSelf>
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     mbar_init(a_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(t_full + i, 1);
-      mbar_init(t_empty + i, 128);
+      mbar_init(t_empty + i, 32 * kTcEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
@@ -211,8 +212,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma_commit(a_empty);  // the A tile may be replaced once every MMA of this unit is done
       }
     }
-  } else {  // ---------------- epilogue: warps 2..5, thread = query row = TMEM lane ----------------
-    const int lq = warp & 3;  // TMEM lane quarter this warp may access
+  } else {  // ---------------- epilogue: thread = query row = TMEM lane, half of the 256 columns ----------------
+    const int lq = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;        // columns [half*128, half*128+128) of every tile
     const int row = lq * 32 + lane;
     uint32_t acc = 0, tphase[2] = {0, 0};
     for (int64_t u = blockIdx.x; u < a.units; u += gridDim.x) {
@@ -226,50 +228,66 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         bv[i] = __int_as_float(0x7F800000);
         bi[i] = kSent;
       }
+      float thr = bv[TC_LIST - 1];
       for (int64_t nb = r0; nb < r1; nb += TC_N) {
         mbar_wait(t_full + acc, tphase[acc]);
         tphase[acc] ^= 1;
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * TC_N;
+        const uint32_t taddr = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * TC_N + half * (TC_N / 2);
 #pragma unroll 1
-        for (int c0 = 0; c0 < TC_N; c0 += 32) {
+        for (int c0 = 0; c0 < TC_N / 2; c0 += 32) {
           uint32_t v[32];
           __syncwarp();
           tmem_ld32(taddr + c0, v);
-          const int64_t cb = nb + c0;
+          const int64_t cb = nb + half * (TC_N / 2) + c0;
           const float nrm = (a.metric == 0 && cb + lane < r1) ? __ldg(a.norms + cb + lane) : 0.f;
-          uint32_t dead = 0;
-          if (kTomb && cb < r1) dead = __ldg(a.tomb + (cb >> 5));
+          // valid columns: inside the split, not deleted, not the query itself
+          uint32_t valid = cb >= r1 ? 0u : (r1 - cb >= 32 ? 0xFFFFFFFFu : ((1u << (uint32_t)(r1 - cb)) - 1u));
+          if (kTomb && cb < r1) valid &= ~__ldg(a.tomb + (cb >> 5));
+          if (kSelf) {
+            const int64_t sj = a.self_base + qi - cb;
+            if (sj >= 0 && sj < 32) valid &= ~(1u << (uint32_t)sj);
+          }
+          // branch-free scores + threshold mask
+          uint32_t pass = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float nj = __shfl_sync(0xffffffffu, nrm, j);
             const float dot = __uint_as_float(v[j]);
-            const float s = a.metric == 0 ? fmaf(-2.f, dot, nj) : -dot;
-            bool ok = (cb + j < r1) && s < bv[TC_LIST - 1];
-            if (kTomb) ok = ok && !((dead >> j) & 1u);
-            if (kSelf) ok = ok && (cb + j != a.self_base + qi);
-            if (ok) {  // insert (s, id) into the ascending register list, dropping the largest
-              const uint32_t id = (uint32_t)(cb + j);
+            const float sc = a.metric == 0 ? fmaf(-2.f, dot, nj) : -dot;
+            v[j] = __float_as_uint(sc);
+            pass |= (sc < thr ? 1u : 0u) << j;
+          }
+          pass &= valid;
+          while (pass) {  // rare after warm-up: insert into the ascending register list
+            const int jj = __ffs(pass) - 1;
+            pass &= pass - 1u;
+            float sc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sc = (j == jj) ? __uint_as_float(v[j]) : sc;
+            if (sc < bv[TC_LIST - 1]) {
+              const uint32_t id = (uint32_t)(cb + jj);
 #pragma unroll
               for (int i = TC_LIST - 1; i > 0; --i) {
-                const bool shift = bv[i - 1] > s;
-                const bool here = !shift && bv[i] > s;
-                bv[i] = shift ? bv[i - 1] : (here ? s : bv[i]);
+                const bool shift = bv[i - 1] > sc;
+                const bool here = !shift && bv[i] > sc;
+                bv[i] = shift ? bv[i - 1] : (here ? sc : bv[i]);
                 bi[i] = shift ? bi[i - 1] : (here ? id : bi[i]);
               }
-              if (bv[0] > s) {
-                bv[0] = s;
+              if (bv[0] > sc) {
+                bv[0] = sc;
                 bi[0] = id;
               }
             }
           }
+          thr = bv[TC_LIST - 1];
         }
         tc_fence_before();
         mbar_arrive(t_empty + acc);
         acc ^= 1;
       }
       if (qi < a.nq) {
-        uint64_t* dst = a.cand + ((size_t)sp * a.nq + qi) * TC_LIST;
+        uint64_t* dst = a.cand + ((size_t)(sp * 2 + half) * a.nq + qi) * TC_LIST;
 #pragma unroll
         for (int i = 0; i < TC_LIST; ++i) dst[i] = bi[i] == kSent ? kEmptyKey : make_key(bv[i], bi[i]);
       }
@@ -470,7 +488,7 @@ size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
   TcPlan p2 = tc_plan(nq, n, dq, 512);
   const int64_t s = std::max(p.splits, p2.splits);
   // cand + norms + facts + fail list + fallback buffers (rows, ids, dists) + FFMA fallback scratch
-  return (size_t)s * nq * TC_LIST * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
+  return (size_t)s * 2 * nq * TC_LIST * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
          (size_t)nq * k * 8 + knn_scratch_bytes(nq, k, n) + 8 * 256;
 }
 
@@ -483,7 +501,7 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   unsigned char* sp = static_cast<unsigned char*>(scratch);
   uint64_t* cand = reinterpret_cast<uint64_t*>(sp);
-  sp += al((size_t)p.splits * nq * TC_LIST * 8);
+  sp += al((size_t)p.splits * 2 * nq * TC_LIST * 8);
   float* norms = reinterpret_cast<float*>(sp);
   sp += al((size_t)n * 4);
   unsigned int* facts = reinterpret_cast<unsigned int*>(sp);  // [0] max norm bits, [1] integral, [2] n_fail
@@ -520,7 +538,7 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   else if (self_base >= 0) e = launch(knn_tc_kernel<false, true>);
   else e = launch(knn_tc_kernel<false, false>);
   if (e != cudaSuccess) return e;
-  knn_rerank_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits, nq, k, vec, dq, Q, q_stride, q_dim,
+  knn_rerank_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride, q_dim,
                                                                metric, facts, out_ids, out_d, fail_list, facts + 2);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // exact FFMA fallback for the queries the certificate rejected
