@@ -35,6 +35,12 @@ struct svf_index {
   double prof_ms[4] = {0, 0, 0, 0};
   int64_t prof_cnt[4] = {0, 0, 0, 0};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int slot;
+  };
+  std::vector<ProfRec> prof_pending;  // recorded without synchronising; resolved by svf_profile_read
+  std::vector<cudaEvent_t> ev_pool;
   std::mutex mu;
 };
 
@@ -133,6 +139,41 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   return true;
 }
 
+cudaEvent_t pool_event(svf_index* idx) {
+  if (!idx->ev_pool.empty()) {
+    cudaEvent_t e = idx->ev_pool.back();
+    idx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_begin(svf_index* idx, cudaStream_t st, cudaEvent_t* a) {
+  *a = nullptr;
+  if (!idx->prof) return;
+  *a = pool_event(idx);
+  cudaEventRecord(*a, st);
+}
+void prof_end(svf_index* idx, cudaStream_t st, cudaEvent_t a, int slot) {
+  if (!idx->prof || !a) return;
+  cudaEvent_t b = pool_event(idx);
+  cudaEventRecord(b, st);
+  idx->prof_pending.push_back({a, b, slot});
+}
+void prof_resolve(svf_index* idx) {
+  for (auto& r : idx->prof_pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    idx->prof_ms[r.slot] += ms;
+    idx->prof_cnt[r.slot] += 1;
+    idx->ev_pool.push_back(r.a);
+    idx->ev_pool.push_back(r.b);
+  }
+  idx->prof_pending.clear();
+}
+
 // run K-S on the index: Q (device) with row stride q_stride and q_dim valid floats
 cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_dim, int64_t nq, uint64_t n_snapshot,
                        uint64_t qidx_base, int L, int n_out, const SearchCfg& c, int p, int max_iter,
@@ -167,33 +208,21 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.smem_per_warp = c.smem_per_warp;
   cudaError_t e = cudaMemsetAsync(idx->small, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  if (idx->prof) cudaEventRecord(idx->ev0, st);
+  cudaEvent_t pa;
+  prof_begin(idx, st, &pa);
   e = launch_search(a, c.kpl, c.cpl, idx->num_sms, st);
   if (e != cudaSuccess) return e;
-  if (idx->prof) {
-    cudaEventRecord(idx->ev1, st);
-    cudaEventSynchronize(idx->ev1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, idx->ev0, idx->ev1);
-    idx->prof_ms[prof_slot] += ms;
-    idx->prof_cnt[prof_slot] += 1;
-  }
+  prof_end(idx, st, pa, prof_slot);
   return cudaSuccess;
 }
 
 template <class F>
 cudaError_t timed(svf_index* idx, int slot, cudaStream_t st, F f) {
-  if (idx->prof) cudaEventRecord(idx->ev0, st);
+  cudaEvent_t pa;
+  prof_begin(idx, st, &pa);
   cudaError_t e = f();
   if (e != cudaSuccess) return e;
-  if (idx->prof) {
-    cudaEventRecord(idx->ev1, st);
-    cudaEventSynchronize(idx->ev1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, idx->ev0, idx->ev1);
-    idx->prof_ms[slot] += ms;
-    idx->prof_cnt[slot] += 1;
-  }
+  prof_end(idx, st, pa, slot);
   return cudaSuccess;
 }
 
@@ -689,6 +718,8 @@ svf_status svf_profile(svf_index* idx, int32_t enable) {
   svf_status s = enter(idx);
   if (s != SVF_OK) return s;
   std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  prof_resolve(idx);
   idx->prof = enable != 0;
   for (int i = 0; i < 4; ++i) {
     idx->prof_ms[i] = 0;
@@ -701,6 +732,8 @@ svf_status svf_profile_read(svf_index* idx, double ms[4], int64_t cnt[4]) {
   svf_status s = enter(idx);
   if (s != SVF_OK) return s;
   std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  prof_resolve(idx);
   for (int i = 0; i < 4; ++i) {
     ms[i] = idx->prof_ms[i];
     cnt[i] = idx->prof_cnt[i];
@@ -729,6 +762,11 @@ svf_status svf_destroy(svf_index* idx) {
   cudaFree(idx->counters);
   if (idx->ev0) cudaEventDestroy(idx->ev0);
   if (idx->ev1) cudaEventDestroy(idx->ev1);
+  for (auto& r : idx->prof_pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : idx->ev_pool) cudaEventDestroy(e);
   cudaGetLastError();
   delete idx;
   return SVF_OK;

@@ -312,11 +312,25 @@ template <int KPL, int CPL, int DQT>
 static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   auto kern = search_kernel<KPL, CPL, DQT>;
   const size_t smem = a.smem_per_warp * kSearchWarpsPerBlock;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // per-instantiation cache of the (smem size -> resident blocks) query: keeps the launch path host-light
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_per_sm = 0;
+  static thread_local int cached_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (cached_smem == smem && cached_dev == dev) {
+    per_sm = cached_per_sm;
+  } else {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
+    if (e != cudaSuccess) return e;
+    cached_smem = smem;
+    cached_per_sm = per_sm;
+    cached_dev = dev;
+  }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long long blocks = (long long)per_sm * num_sms;
   const long long need = (a.nq + kSearchWarpsPerBlock - 1) / kSearchWarpsPerBlock;
