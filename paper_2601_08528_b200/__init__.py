@@ -121,6 +121,13 @@ class Index:
         check(lib().svf_search(self._h, qp, nq, k, itopk, ip, dp, _stream(dev)))
         return ids, d
 
+    def search_into(self, Q, k: int, itopk: int, out_ids, out_dists):
+        """svf_search into caller-owned CUDA tensors (no allocation: safe inside CUDA-graph capture)."""
+        qp, qk, dev = _prep(Q, np.float32, torch.float32 if torch else None)
+        check(lib().svf_search(self._h, qp, int(qk.shape[0]), k, itopk, out_ids.data_ptr(), out_dists.data_ptr(),
+                               _stream(dev)))
+        return out_ids, out_dists
+
     def insert(self, X):
         """Insert(x) for a batch (svf_insert).  Returns the assigned ids (numpy uint32)."""
         xp, xk, dev = _prep(X, np.float32, torch.float32 if torch else None)
