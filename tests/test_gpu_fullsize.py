@@ -1,0 +1,92 @@
+"""Full-size parity at BASELINE.json configs[1] (C2: 1M x 128 integer-valued G-LM, R=64, 10K-query batch), in the
+launch configuration bench.py times (same build parameters, itopk from the bench sweep range, graph replay not
+needed for correctness).  The oracle computes sampled outputs one by one; integer data => bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import base_rows, pack_tomb, query_rows
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+SENT = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def c2():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2601_08528_b200 as svf
+
+    X = base_rows("C2")
+    Q = query_rows("C2")
+    Xnew = base_rows("C2", 1_000_000, 10_000)
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, capacity=1_010_000)
+    return svf, idx, X, Q, Xnew
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def test_c2_graph_invariants(c2):
+    svf, idx, X, Q, _ = c2
+    st = idx.export()
+    g = st["graph"]
+    assert g.shape == (1_000_000, 64) and np.all(g != SENT)            # fixed degree R, N >> R
+    assert not np.any(g == np.arange(len(g), dtype=np.uint32)[:, None])  # no self loops
+    srt = np.sort(g, axis=1)
+    assert not np.any(srt[:, 1:] == srt[:, :-1])                        # no duplicates
+    ed = st["edge_dist"]
+    tail = ed[:, 32:]
+    assert np.all(np.diff(tail, axis=1) >= 0)                          # tail sorted by distance (no deletions yet)
+    rows = np.random.default_rng(0).choice(len(g), 200, replace=False)
+    for v in rows:                                                      # stored distances are the true distances
+        ref = ((X[g[v]].astype(np.float64) - X[v]) ** 2).sum(1)
+        assert np.array_equal(ed[v], ref.astype(np.float32))
+    indeg = np.bincount(g.ravel().astype(np.int64), minlength=len(g))
+    assert indeg.sum() == g.size and (indeg == 0).mean() < 0.02
+
+
+@pytest.mark.parametrize("L", [14, 32])
+def test_c2_search_sampled_bit_exact(c2, L):
+    svf, idx, X, Q, _ = c2
+    ids, d = idx.search(torch.from_numpy(Q).cuda(), 10, L)
+    ids, d = u32(ids), d.cpu().numpy()
+    st = idx.export()
+    sample = np.random.default_rng(L).choice(len(Q), 400, replace=False)
+    ri, rd, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, qidx=sample)
+    assert np.array_equal(ids[sample], ri) and np.array_equal(d[sample], rd)
+
+
+def test_c2_exact_knn_sampled(c2):
+    svf, idx, X, Q, _ = c2
+    gi, gd = idx.knn_exact(torch.from_numpy(Q).cuda(), 10)
+    assert idx.knn_stats()["fallbacks"] == 0
+    sample = np.random.default_rng(7).choice(len(Q), 24, replace=False)
+    ri, rd = oracle.bf_knn(X, Q[sample], 10)
+    assert np.array_equal(u32(gi)[sample], ri) and np.array_equal(gd.cpu().numpy()[sample], rd)
+
+
+def test_c2_insert_and_delete_whole_graph_bit_exact(c2):
+    """Insert 1% (10K) then delete 1%: the whole 1M-row adjacency equals the oracle's O3 on the same state."""
+    svf, idx, X, Q, Xnew = c2
+    st0 = idx.export()
+    n0 = st0["n_alloc"]
+    dead = np.random.default_rng(3).choice(n0, 10_000, replace=False).astype(np.uint32)
+    assert idx.delete(torch.from_numpy(dead.view(np.int32)).cuda()) == 10_000
+    new_ids = idx.insert(torch.from_numpy(Xnew).cuda())
+    assert np.array_equal(new_ids, np.arange(n0, n0 + len(Xnew), dtype=np.uint32))
+    st1 = idx.export()
+    cap = n0 + len(Xnew)
+    G = np.vstack([st0["graph"], np.full((len(Xnew), 64), SENT, np.uint32)])
+    E = np.vstack([st0["edge_dist"], np.full((len(Xnew), 64), np.inf, np.float32)])
+    Xall = np.vstack([X, Xnew])
+    gr, er = oracle.insert(Xall, G, E, n_alloc=n0, n_new=len(Xnew), P=32, L_ins=128, B_ins=4096,
+                           tomb=pack_tomb(dead, cap))
+    assert np.array_equal(st1["graph"], gr)
+    assert np.array_equal(st1["edge_dist"], er)
+    assert np.array_equal(st1["tomb"], pack_tomb(dead, cap)[: len(st1["tomb"])])
+    # deleted ids are never returned by a full-batch search afterwards
+    ids, _ = idx.search(torch.from_numpy(Q).cuda(), 10, 16)
+    assert not np.isin(u32(ids), dead).any()
