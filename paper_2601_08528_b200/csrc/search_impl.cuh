@@ -191,6 +191,8 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
     for (int r = 0; r < KPL; ++r) pool[r] = kEmptyKey;
     int hcount = 0;
     uint32_t n_dist = 0, iters = 0, n_exp = 0;
+    uint32_t spec_id = kSent;  // parent whose row sits in spec_row (speculative next-row load)
+    uint32_t spec_row[CPL];
 
     // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
     const uint64_t n = a.n_alloc;
@@ -248,34 +250,54 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
       }
       if (np == 0) break;
       __syncwarp();
-      // speculative: the best still-unparented entry is the likely next parent; pull its row toward L2 while
-      // this iteration's rows and vectors are in flight (a miss costs nothing but a prefetch)
-      {
-        uint64_t nxt = kEmptyKey;
+      // The best still-unparented entry is the likely next parent (it stays first unless this iteration's
+      // candidates beat it).  p == 1: load its row into registers now, consumed next iteration if the guess holds,
+      // so the dependent row fetch overlaps this iteration's vector gathers.  p > 1: pull it toward L2.
+      uint64_t nxt = kEmptyKey;
 #pragma unroll
-        for (int r = KPL - 1; r >= 0; --r) {
-          const unsigned m = __ballot_sync(0xffffffffu, (pool[r] & 1ull) == 0ull);
-          if (m) nxt = __shfl_sync(0xffffffffu, pool[r], __ffs(m) - 1);
-        }
-        if (nxt != kEmptyKey && lane < ((a.R * 4 + 127) >> 7)) {
-          const uint32_t* prow = a.graph + (size_t)key_id(nxt) * a.R + lane * 32;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(prow));
-        }
+      for (int r = KPL - 1; r >= 0; --r) {
+        const unsigned m = __ballot_sync(0xffffffffu, (pool[r] & 1ull) == 0ull);
+        if (m) nxt = __shfl_sync(0xffffffffu, pool[r], __ffs(m) - 1);
       }
       ++iters;
       n_exp += np;
       const int ncand = np * a.R;
       if (hcount + ncand > H / 2) hcount = hash_reset<KPL>(tab, a.hbits, pool, lane);
-      // S3: neighbour rows (coalesced), S4: sentinel / snapshot / tombstone / visited filters
+      // S3: neighbour rows (coalesced; from the speculative registers when the guess was right)
+      uint32_t rowv[CPL];
+      if (np == 1 && spar[0] == spec_id) {
+#pragma unroll
+        for (int r = 0; r < CPL; ++r) rowv[r] = spec_row[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < CPL; ++r) {
+          const int e = r * 32 + lane;
+          rowv[r] = kSent;
+          if (e < ncand) {
+            const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
+            rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
+          }
+        }
+      }
+      spec_id = kSent;
+      if (nxt != kEmptyKey) {
+        if (a.p == 1) {
+          spec_id = key_id(nxt);
+#pragma unroll
+          for (int r = 0; r < CPL; ++r) {
+            const int e = r * 32 + lane;
+            spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
+          }
+        } else if (lane < ((a.R * 4 + 127) >> 7)) {
+          const uint32_t* prow = a.graph + (size_t)key_id(nxt) * a.R + lane * 32;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(prow));
+        }
+      }
+      // S4: sentinel / snapshot / tombstone / visited filters
       int running = 0;
 #pragma unroll
       for (int r = 0; r < CPL; ++r) {
-        const int e = r * 32 + lane;
-        uint32_t id = kSent;
-        if (e < ncand) {
-          const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
-          id = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
-        }
+        const uint32_t id = rowv[r];
         bool ok = id != kSent && (uint64_t)id < n;
         if (ok) ok = !tomb_dead(a.tomb, id);
         if (ok) ok = hash_insert(tab, a.hbits, id);
