@@ -13,7 +13,7 @@ SOURCES = ["index.cu", "search.cu", "search_d0.cu", "search_d24.cu", "search_d32
 HEADERS = ["common.cuh", "kernels.h", "search_impl.cuh", os.path.join("..", "..", "include", "svf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("SVF_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:

@@ -8,7 +8,10 @@ namespace svf {
 
 constexpr int kSearchWarpsPerBlock = 4;
 // register cap per pool size: small pools -> more resident warps (latency-bound gathers want occupancy)
-constexpr int search_min_blocks(int kpl) { return kpl <= 1 ? 6 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2; }
+#ifndef SVF_MINB1
+#define SVF_MINB1 6
+#endif
+constexpr int search_min_blocks(int kpl) { return kpl <= 1 ? SVF_MINB1 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2; }
 
 struct SearchArgs {
   const float* vec;        // [cap][dq*4]
