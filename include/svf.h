@@ -124,6 +124,11 @@ svf_status svf_import(const svf_params* p, const float* vec, const uint32_t* gra
 svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* cand_ids, const float* cand_d,
                                int64_t n_new, int32_t n_cand, void* stream);
 
+/* Warps serving one query in svf_search / svf_insert's search: 1, 2 (both warps keep identical pools and split the
+ * candidate slots: same results, about half the per-query latency), or 0 = automatic (2 for batches up to ~6
+ * queries per resident warp when the slots split evenly, else 1).  Results are identical for every setting. */
+svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq);
+
 /* Exact-kNN engine: mode 0 = automatic (tcgen05 TF32 scoring + exact FFMA re-rank with a certificate, exact FFMA
  * fallback for rejected queries; used when k <= 32 and query rows are 16-byte aligned), 1 = FFMA tiles only. */
 svf_status svf_set_knn_mode(svf_index* idx, int32_t mode);

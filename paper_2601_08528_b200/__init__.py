@@ -183,6 +183,10 @@ class Index:
         check(lib().svf_last_search_counters(self._h, out))
         return {"n_dist": out[0], "iters": out[1], "n_exp": out[2], "queries": out[3]}
 
+    def set_warps_per_query(self, wpq: int):
+        """1 or 2 warps per query (identical results), 0 = automatic."""
+        check(lib().svf_set_warps_per_query(self._h, wpq))
+
     def set_knn_mode(self, mode: int):
         """0 = tcgen05 TF32 scoring + exact re-rank (auto), 1 = FFMA tiles only."""
         check(lib().svf_set_knn_mode(self._h, mode))

@@ -30,6 +30,7 @@ struct svf_index {
   bool poisoned = false;
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
   int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
+  int wpq = 0;                          // warps per query: 0 auto, 1, 2
   uint64_t knn_queries = 0, knn_fallbacks = 0, knn_tc_calls = 0;
   bool prof = false;
   double prof_ms[4] = {0, 0, 0, 0};
@@ -113,8 +114,7 @@ int pow2_at_least(int x) {
 }
 
 struct SearchCfg {
-  int kpl, cpl, hbits, team, nv, n_init;
-  size_t smem_per_warp;
+  int kpl, cpl, hbits, team, nv, n_init, wpq;
 };
 
 bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, SearchCfg& c, std::string& why) {
@@ -135,7 +135,7 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
   c.n_init = n_init > 0 ? n_init : L;
-  c.smem_per_warp = search_smem_per_warp(idx->dq, MP, c.hbits);
+  c.wpq = idx->wpq == 2 ? 2 : 1;
   return true;
 }
 
@@ -205,7 +205,10 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_d = out_d;
   a.counters = counters;
   a.work_counter = idx->small;
-  a.smem_per_warp = c.smem_per_warp;
+  // pair mode (2 warps per query) halves per-query latency; worth it while the batch does not oversubscribe
+  // the resident warps many times (auto: nq below ~6 queries per resident warp slot)
+  a.wpq = c.wpq;
+  if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && nq <= 6LL * idx->num_sms * 24) ? 2 : 1;
   cudaError_t e = cudaMemsetAsync(idx->small, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   cudaEvent_t pa;
@@ -692,6 +695,15 @@ svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
     out[1] += h[q * 3 + 1];
     out[2] += h[q * 3 + 2];
   }
+  return SVF_OK;
+}
+
+svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (wpq < 0 || wpq > 2) return fail(SVF_ERR_INVALID, "warps_per_query must be 0 (auto), 1 or 2");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->wpq = wpq;
   return SVF_OK;
 }
 

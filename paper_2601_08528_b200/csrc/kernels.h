@@ -35,10 +35,8 @@ struct SearchArgs {
   float* out_d;
   uint32_t* counters;      // nullable: [nq][3] = n_dist, iters, n_exp
   unsigned long long* work_counter;  // zeroed before launch
-  size_t smem_per_warp;
+  int wpq;                 // warps per query: 1, or 2 (pair mode; used when the candidate slots split evenly)
 };
-
-size_t search_smem_per_warp(int dq, int mp, int hbits);
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 
 // K-L1: detour-ranked forward rows for new ids [first, first + n_new) from candidates [n_new][nc]

@@ -8,11 +8,6 @@ cudaError_t launch_search_d24(SearchArgs a, int kpl, int cpl, int num_sms, cudaS
 cudaError_t launch_search_d32(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 cudaError_t launch_search_d50(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 
-size_t search_smem_per_warp(int dq, int mp, int hbits) {
-  size_t b = (size_t)dq * 16 + (size_t)mp * 8 + (size_t)mp * 4 + 8 * 4 + ((size_t)4 << hbits);
-  return (b + 15) & ~(size_t)15;
-}
-
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st) {
   switch (a.dq) {
     case 24: return launch_search_d24(a, kpl, cpl, num_sms, st);   // D = 96 (Deep-shaped)

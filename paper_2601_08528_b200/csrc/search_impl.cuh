@@ -1,14 +1,16 @@
 // K-S: batched greedy graph search on sm_100a (Algorithm 1).
 //
-// Design (DESIGN.md §"K-S"): one WARP per query, persistent warps pulling queries from an atomic counter.
+// Design (DESIGN.md §6 "K-S"): persistent blocks of 4 warps pull query ids from an atomic counter; each query is
+// served by WPQ warps (1, or 2 to halve per-query latency so a 10K batch does not end in a long tail).
 //  - pool (the paper's candidate list C_i) lives in registers as 64-bit keys (dist, id, parent flag),
-//    striped over the warp (element e = r*32 + lane), exact size L (I6) inside a power-of-two buffer;
-//  - visited set = per-warp open-addressing table in shared memory, "forgetful": when it reaches half load it
-//    is cleared and the pool ids are re-registered, which provably leaves results unchanged (I7);
-//  - distances: teams of T lanes per vector, each lane loads NV coalesced 16-byte chunks of the row, FFMA,
-//    xor-shuffle reduction inside the team;
-//  - merge: bitonic sort of the candidate keys + bitonic merge into the pool (warp shuffles only).
-// No __syncthreads: the warps of a block are independent; all intra-query sync is __syncwarp.
+//    striped over the warp (element e = r*32 + lane), exact size L (I6) inside a power-of-two buffer.  With
+//    WPQ = 2 both warps hold identical pools: every step that changes the pool is computed identically by both;
+//  - visited set = per-query open-addressing table in shared memory, "forgetful": at half load it is cleared and
+//    the pool ids are re-registered, which provably leaves results unchanged (I7);
+//  - candidate slots are split between the query's warps (register r of the candidate array belongs to warp
+//    r % WPQ): each warp filters, hashes and scores its slots (teams of T lanes per vector, coalesced 16-byte
+//    gathers, FFMA, xor-shuffle reduction) and drops keys not better than the pool's L-th; one pair barrier per
+//    iteration, then every warp sorts the union (bitonic) and merges it into its pool (bitonic merge).
 #pragma once
 #include "common.cuh"
 #include "kernels.h"
@@ -28,20 +30,30 @@ __device__ __forceinline__ bool hash_insert(uint32_t* tab, int hbits, uint32_t i
   }
 }
 
-template <int KPL>
-__device__ __forceinline__ int hash_reset(uint32_t* tab, int hbits, const uint64_t (&pool)[KPL], int lane) {
-  __syncwarp();
+template <int WPQ>
+__device__ __forceinline__ void qsync(int slot) {
+  if (WPQ == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * WPQ) : "memory");
+  }
+}
+
+// clear the table and re-register the pool ids (I7); identical decision in every warp of the query
+template <int KPL, int WPQ>
+__device__ __forceinline__ int hash_reset(uint32_t* tab, int hbits, const uint64_t (&pool)[KPL], int lane, int h,
+                                          int slot) {
   const int H = 1 << hbits;
-  for (int i = lane; i < H; i += 32) tab[i] = kHashEmpty;
-  __syncwarp();
+  for (int i = h * 32 + lane; i < H; i += 32 * WPQ) tab[i] = kHashEmpty;
+  qsync<WPQ>(slot);
   int cnt = 0;
 #pragma unroll
   for (int r = 0; r < KPL; ++r) {
     const bool v = pool[r] != kEmptyKey;
-    if (v) hash_insert(tab, hbits, key_id(pool[r]));
+    if (v && h == 0) hash_insert(tab, hbits, key_id(pool[r]));
     cnt += __popc(__ballot_sync(0xffffffffu, v));
   }
-  __syncwarp();
+  qsync<WPQ>(slot);
   return cnt;
 }
 
@@ -53,10 +65,11 @@ struct Geo {
   static constexpr int NV = (DQT + T - 1) / T;
 };
 
-// Distances for the S survivors listed in sid[0..S) -> skey[0..S); then sort + merge into the pool.
+// Distances of this warp's S survivors sid[0..S) -> keys; keep those strictly better than the pool's current L-th
+// key (the only ones that can enter: the pool keeps the L smallest of pool U cand), compacted into skey[0..S2).
 template <int KPL, int CPL, int DQT>
-__device__ __forceinline__ void score_and_merge(const SearchArgs& a, uint64_t (&pool)[KPL], const uint32_t* sid,
-                                                uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
+__device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
+                                         uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
   constexpr int U = 2;
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
@@ -109,41 +122,54 @@ __device__ __forceinline__ void score_and_merge(const SearchArgs& a, uint64_t (&
     }
   }
   __syncwarp();
-  // Only candidates strictly better than the pool's current L-th key can enter (exact: the pool keeps the L
-  // smallest of pool U cand).  Drop the rest before sorting; most iterations keep only a handful.
   uint64_t kreg = kEmptyKey;
 #pragma unroll
   for (int r = 0; r < KPL; ++r)
     if (r == ((a.L - 1) >> 5)) kreg = pool[r];
   const uint64_t kth = __shfl_sync(0xffffffffu, kreg, (a.L - 1) & 31);
   uint64_t c[CPL];
-  int S2 = 0;
 #pragma unroll
   for (int r = 0; r < CPL; ++r) {
     const int e = r * 32 + lane;
-    c[r] = e < S ? skey[e] : kEmptyKey;
-    const bool pass = c[r] < kth;
-    c[r] = pass ? c[r] : kEmptyKey;
-    S2 += __popc(__ballot_sync(0xffffffffu, pass));
+    c[r] = (e < S && skey[e] < kth) ? skey[e] : kEmptyKey;
   }
-  if (S2 == 0) return;
-  if (S2 <= 32) {
-    // compact the survivors into one register (through shared memory) and use a 32-wide sort
-    __syncwarp();
-    int base2 = 0;
+  __syncwarp();
+  int S2 = 0;
 #pragma unroll
-    for (int r = 0; r < CPL; ++r) {
-      const bool pass = c[r] != kEmptyKey;
-      const unsigned m = __ballot_sync(0xffffffffu, pass);
-      if (pass) skey[base2 + __popc(m & ((1u << lane) - 1u))] = c[r];
-      base2 += __popc(m);
+  for (int r = 0; r < CPL; ++r) {
+    const bool pass = c[r] != kEmptyKey;
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    if (pass) skey[S2 + __popc(m & ((1u << lane) - 1u))] = c[r];
+    S2 += __popc(m);
+  }
+  return S2;
+}
+
+// Merge the union of the query's warps' surviving keys (list w = skeys[w][0..cnt[w])) into the pool.
+template <int KPL, int CPL, int WPQ>
+__device__ __forceinline__ void merge_all(const SearchArgs& a, uint64_t (&pool)[KPL], uint64_t* const (&lists)[WPQ],
+                                          const int (&cnt)[WPQ], int total, int lane) {
+  auto at = [&](int e) -> uint64_t {
+    int off = 0;
+#pragma unroll
+    for (int w = 0; w < WPQ; ++w) {
+      if (e - off < cnt[w]) return lists[w][e - off];
+      off += cnt[w];
     }
-    __syncwarp();
+    return kEmptyKey;
+  };
+  if (total <= 32) {
     uint64_t c1[1];
-    c1[0] = lane < S2 ? skey[lane] : kEmptyKey;
+    c1[0] = lane < total ? at(lane) : kEmptyKey;
     warp_sort<1>(c1, lane);
     warp_merge_into<KPL, 1>(pool, c1, lane);
   } else {
+    uint64_t c[CPL];
+#pragma unroll
+    for (int r = 0; r < CPL; ++r) {
+      const int e = r * 32 + lane;
+      c[r] = e < total ? at(e) : kEmptyKey;
+    }
     warp_sort<CPL>(c, lane);
     warp_merge_into<KPL, CPL>(pool, c, lane);
   }
@@ -152,47 +178,97 @@ __device__ __forceinline__ void score_and_merge(const SearchArgs& a, uint64_t (&
     if (r * 32 + lane >= a.L) pool[r] = kEmptyKey;  // exact pool size L (I6)
 }
 
-template <int KPL, int CPL, int DQT>
+template <int CPL, int WPQ>
+struct Smem {
+  static constexpr int MP = 32 * CPL;
+  // per warp: survivor ids [MP], keys [2 parities][MP], counts [2 parities][2]
+  static constexpr size_t warp_bytes = ((size_t)MP * 4 + (size_t)2 * MP * 8 + 16 + 15) & ~(size_t)15;
+  // per query slot: visited table [2^hbits], parents [WPQ][8], query id
+  static size_t __host__ __device__ slot_bytes(int hbits) {
+    return (((size_t)4 << hbits) + (size_t)WPQ * 8 * 4 + 16 + 15) & ~(size_t)15;
+  }
+  static size_t __host__ __device__ block_bytes(int hbits) {
+    return (size_t)(kSearchWarpsPerBlock / WPQ) * slot_bytes(hbits) + kSearchWarpsPerBlock * warp_bytes;
+  }
+};
+
+template <int KPL, int CPL, int DQT, int WPQ>
 __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int MP = 32 * CPL;
+  using SM = Smem<CPL, WPQ>;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* base = smem + (size_t)wib * a.smem_per_warp;
-  float4* qs = reinterpret_cast<float4*>(base);
-  uint64_t* skey = reinterpret_cast<uint64_t*>(base + (size_t)a.dq * 16);
-  uint32_t* sid = reinterpret_cast<uint32_t*>(skey + MP);
-  uint32_t* spar = sid + MP;  // parents of the current iteration (<= 8)
-  uint32_t* tab = spar + 8;
+  const int slot = wib / WPQ, h = wib % WPQ;
+  unsigned char* sbase = smem + (size_t)slot * SM::slot_bytes(a.hbits);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(sbase);
+  uint32_t* spar = tab + (1 << a.hbits) + h * 8;  // this warp's copy of the iteration's parents
+  unsigned long long* qslot =
+      reinterpret_cast<unsigned long long*>(sbase + SM::slot_bytes(a.hbits) - 16);
+  unsigned char* wbase[WPQ];
+#pragma unroll
+  for (int w = 0; w < WPQ; ++w)
+    wbase[w] = smem + (size_t)(kSearchWarpsPerBlock / WPQ) * SM::slot_bytes(a.hbits) +
+               (size_t)(slot * WPQ + w) * SM::warp_bytes;
+  uint32_t* sid = reinterpret_cast<uint32_t*>(wbase[h]);
   const int H = 1 << a.hbits;
   const int T = DQT ? Geo<DQT>::T : a.team;
   const int tl = lane & (T - 1);
+  auto keys_of = [&](int w, int par) { return reinterpret_cast<uint64_t*>(wbase[w] + (size_t)MP * 4) + par * MP; };
+  auto cnts_of = [&](int w) { return reinterpret_cast<int*>(wbase[w] + (size_t)MP * 4 + (size_t)2 * MP * 8); };
 
   for (;;) {
-    unsigned long long qi = 0;
-    if (lane == 0) qi = atomicAdd(a.work_counter, 1ull);
-    qi = __shfl_sync(0xffffffffu, qi, 0);
+    if (h == 0 && lane == 0) *qslot = atomicAdd(a.work_counter, 1ull);
+    qsync<WPQ>(slot);
+    const unsigned long long qi = *qslot;
     if (qi >= (unsigned long long)a.nq) break;
 
-    // S0: stage the query (zero-padded to Dp) and clear the visited table
+    // S0: the query fragment this lane needs (zero-padded to Dp), straight from global memory; clear the table
     const float* qg = a.Q + (size_t)qi * a.q_stride;
-    float* qsf = reinterpret_cast<float*>(qs);
-    for (int i = lane; i < a.dq * 4; i += 32) qsf[i] = i < a.q_dim ? __ldg(qg + i) : 0.f;
-    for (int i = lane; i < H; i += 32) tab[i] = kHashEmpty;
-    __syncwarp();
     float4 qv[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int c = tl + T * v;
-      qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? qs[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float f[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = c * 4 + j;
+        f[j] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq && i < a.q_dim) ? __ldg(qg + i) : 0.f;
+      }
+      qv[v] = make_float4(f[0], f[1], f[2], f[3]);
     }
+    for (int i = h * 32 + lane; i < H; i += 32 * WPQ) tab[i] = kHashEmpty;
+    qsync<WPQ>(slot);
     uint64_t pool[KPL];
 #pragma unroll
     for (int r = 0; r < KPL; ++r) pool[r] = kEmptyKey;
-    int hcount = 0;
+    int hcount = 0, par = 0;
     uint32_t n_dist = 0, iters = 0, n_exp = 0;
     uint32_t spec_id = kSent;  // parent whose row sits in spec_row (speculative next-row load)
     uint32_t spec_row[CPL];
+
+    // exchange the warps' survivor lists and merge (one barrier per step)
+    auto exchange_merge = [&](int S_own, int S2_own) {
+      if (lane == 0) {
+        cnts_of(h)[par * 2 + 0] = S_own;
+        cnts_of(h)[par * 2 + 1] = S2_own;
+      }
+      qsync<WPQ>(slot);
+      int cnt[WPQ];
+      uint64_t* lists[WPQ];
+      int total = 0, raw = 0;
+#pragma unroll
+      for (int w = 0; w < WPQ; ++w) {
+        raw += cnts_of(w)[par * 2 + 0];
+        cnt[w] = cnts_of(w)[par * 2 + 1];
+        lists[w] = keys_of(w, par);
+        total += cnt[w];
+      }
+      hcount += raw;
+      n_dist += raw;
+      if (total > 0) merge_all<KPL, CPL, WPQ>(a, pool, lists, cnt, total, lane);
+      par ^= 1;
+    };
 
     // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
     const uint64_t n = a.n_alloc;
@@ -206,8 +282,8 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
       const uint32_t step32 = (uint32_t)((pa * 32ull) % n);
       int taken = 0;
       for (uint64_t j0 = 0; j0 < n && taken < a.n_init; j0 += MP) {
-        if (hcount + MP > H / 2) hcount = hash_reset<KPL>(tab, a.hbits, pool, lane);
-        int running = 0;
+        if (hcount + MP > H / 2) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
+        int running = 0, mine = 0;
 #pragma unroll
         for (int r = 0; r < CPL; ++r) {
           const uint64_t j = j0 + (uint64_t)(r * 32 + lane);
@@ -217,18 +293,20 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
           bool ok = j < n;
           if (ok) ok = !tomb_dead(a.tomb, id);
           const unsigned m = __ballot_sync(0xffffffffu, ok);
-          const int rank = taken + running + __popc(m & ((1u << lane) - 1u));
-          if (ok && rank < a.n_init) {
-            sid[rank - taken] = id;
+          const int pos = running + __popc(m & ((1u << lane) - 1u));  // position among this chunk's live ids
+          const bool keep = ok && taken + pos < a.n_init && ((pos >> 5) % WPQ) == h;
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            sid[mine + __popc(km & ((1u << lane) - 1u))] = id;
             hash_insert(tab, a.hbits, id);
           }
+          mine += __popc(km);
           running += __popc(m);
         }
         const int kept = min(running, a.n_init - taken);
         taken += kept;
-        hcount += kept;
-        n_dist += kept;
-        score_and_merge<KPL, CPL, DQT>(a, pool, sid, skey, kept, qv, lane);
+        const int S2 = score_own<KPL, CPL, DQT>(a, pool, sid, keys_of(h, par), mine, qv, lane);
+        exchange_merge(mine, S2);
       }
     }
 
@@ -262,21 +340,21 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
       ++iters;
       n_exp += np;
       const int ncand = np * a.R;
-      if (hcount + ncand > H / 2) hcount = hash_reset<KPL>(tab, a.hbits, pool, lane);
-      // S3: neighbour rows (coalesced; from the speculative registers when the guess was right)
+      if (hcount + ncand > H / 2) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
+      // S3: this warp's neighbour-row slots (registers r with r % WPQ == h), coalesced; from the speculative
+      // registers when the guess was right
       uint32_t rowv[CPL];
-      if (np == 1 && spar[0] == spec_id) {
+      const bool hit = np == 1 && spar[0] == spec_id;
 #pragma unroll
-        for (int r = 0; r < CPL; ++r) rowv[r] = spec_row[r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < CPL; ++r) {
-          const int e = r * 32 + lane;
-          rowv[r] = kSent;
-          if (e < ncand) {
-            const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
-            rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
-          }
+      for (int r = 0; r < CPL; ++r) {
+        const int e = r * 32 + lane;
+        rowv[r] = kSent;
+        if ((r % WPQ) != h) continue;
+        if (hit) {
+          rowv[r] = spec_row[r];
+        } else if (e < ncand) {
+          const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
+          rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
         }
       }
       spec_id = kSent;
@@ -286,17 +364,18 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
 #pragma unroll
           for (int r = 0; r < CPL; ++r) {
             const int e = r * 32 + lane;
-            spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
+            if ((r % WPQ) == h) spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
           }
-        } else if (lane < ((a.R * 4 + 127) >> 7)) {
+        } else if (h == 0 && lane < ((a.R * 4 + 127) >> 7)) {
           const uint32_t* prow = a.graph + (size_t)key_id(nxt) * a.R + lane * 32;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(prow));
         }
       }
-      // S4: sentinel / snapshot / tombstone / visited filters
+      // S4: sentinel / snapshot / tombstone / visited filters on this warp's slots
       int running = 0;
 #pragma unroll
       for (int r = 0; r < CPL; ++r) {
+        if ((r % WPQ) != h) continue;
         const uint32_t id = rowv[r];
         bool ok = id != kSent && (uint64_t)id < n;
         if (ok) ok = !tomb_dead(a.tomb, id);
@@ -305,24 +384,26 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
         if (ok) sid[running + __popc(m & ((1u << lane) - 1u))] = id;
         running += __popc(m);
       }
-      hcount += running;
-      n_dist += running;
-      if (running > 0) score_and_merge<KPL, CPL, DQT>(a, pool, sid, skey, running, qv, lane);
+      // S5: distances of this warp's survivors; S6: exchange + merge
+      const int S2 = score_own<KPL, CPL, DQT>(a, pool, sid, keys_of(h, par), running, qv, lane);
+      exchange_merge(running, S2);
     }
 
     // S8: emit the first n_out entries (k, or the whole pool in insert mode)
+    if (h == 0) {
 #pragma unroll
-    for (int r = 0; r < KPL; ++r) {
-      const int e = r * 32 + lane;
-      if (e < a.n_out) {
-        a.out_ids[(size_t)qi * a.n_out + e] = key_id(pool[r]);
-        a.out_d[(size_t)qi * a.n_out + e] = key_dist(pool[r]);
+      for (int r = 0; r < KPL; ++r) {
+        const int e = r * 32 + lane;
+        if (e < a.n_out) {
+          a.out_ids[(size_t)qi * a.n_out + e] = key_id(pool[r]);
+          a.out_d[(size_t)qi * a.n_out + e] = key_dist(pool[r]);
+        }
       }
-    }
-    if (a.counters != nullptr && lane == 0) {
-      a.counters[qi * 3 + 0] = n_dist;
-      a.counters[qi * 3 + 1] = iters;
-      a.counters[qi * 3 + 2] = n_exp;
+      if (a.counters != nullptr && lane == 0) {
+        a.counters[qi * 3 + 0] = n_dist;
+        a.counters[qi * 3 + 1] = iters;
+        a.counters[qi * 3 + 2] = n_exp;
+      }
     }
     __syncwarp();
   }
@@ -330,10 +411,10 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
 
 }  // namespace
 
-template <int KPL, int CPL, int DQT>
+template <int KPL, int CPL, int DQT, int WPQ>
 static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
-  auto kern = search_kernel<KPL, CPL, DQT>;
-  const size_t smem = a.smem_per_warp * kSearchWarpsPerBlock;
+  auto kern = search_kernel<KPL, CPL, DQT, WPQ>;
+  const size_t smem = Smem<CPL, WPQ>::block_bytes(a.hbits);
   // per-instantiation cache of the (smem size -> resident blocks) query: keeps the launch path host-light
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0;
@@ -355,20 +436,30 @@ static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long long blocks = (long long)per_sm * num_sms;
-  const long long need = (a.nq + kSearchWarpsPerBlock - 1) / kSearchWarpsPerBlock;
+  constexpr int qpb = kSearchWarpsPerBlock / WPQ;
+  const long long need = (a.nq + qpb - 1) / qpb;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, kSearchWarpsPerBlock * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
+template <int KPL, int CPL, int DQT>
+static cudaError_t launch_wpq(SearchArgs a, int num_sms, cudaStream_t st) {
+  // two warps per query only where the candidate slots split evenly (CPL >= 2) and pools are small
+  if constexpr (CPL >= 2 && KPL <= 4) {
+    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2>(a, num_sms, st);
+  }
+  return launch_kpl_cpl<KPL, CPL, DQT, 1>(a, num_sms, st);
+}
+
 template <int KPL, int DQT>
 static cudaError_t launch_kpl(SearchArgs a, int cpl, int num_sms, cudaStream_t st) {
   switch (cpl) {
-    case 1: return launch_kpl_cpl<KPL, 1, DQT>(a, num_sms, st);
-    case 2: return launch_kpl_cpl<KPL, 2, DQT>(a, num_sms, st);
-    case 4: return launch_kpl_cpl<KPL, 4, DQT>(a, num_sms, st);
-    case 8: return launch_kpl_cpl<KPL, 8, DQT>(a, num_sms, st);
+    case 1: return launch_wpq<KPL, 1, DQT>(a, num_sms, st);
+    case 2: return launch_wpq<KPL, 2, DQT>(a, num_sms, st);
+    case 4: return launch_wpq<KPL, 4, DQT>(a, num_sms, st);
+    case 8: return launch_wpq<KPL, 8, DQT>(a, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -54,10 +54,13 @@ def c1():
 
 
 # ---- K-S search ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("L,p", [(16, 1), (32, 1), (64, 1), (128, 1), (256, 1), (48, 2), (100, 4), (512, 1)])
-def test_search_bit_exact_integer_data(svf, c1, L, p):
+@pytest.mark.parametrize("L,p,wpq", [(16, 1, 1), (16, 1, 2), (32, 1, 1), (32, 2, 2), (64, 1, 2), (128, 1, 1),
+                                     (128, 1, 2), (256, 1, 0), (48, 2, 1), (100, 4, 2), (512, 1, 0)])
+def test_search_bit_exact_integer_data(svf, c1, L, p, wpq):
+    """wpq = warps per query (1, 2 = pair mode with split candidate slots, 0 = auto): identical results."""
     X, Q, g, e = c1
     idx = svf.Index.from_state(X, g, e, search_width=p)
+    idx.set_warps_per_query(wpq)
     idx.set_search_params(p, 0, 0, 13 if L <= 128 else 0)   # a table >= 2x the visits: few recomputes
     k = min(10, L)
     ids, d = idx.search(cuda(Q), k, L)
@@ -71,11 +74,12 @@ def test_search_bit_exact_integer_data(svf, c1, L, p):
     assert cnt["n_dist"] <= (1.05 if L <= 128 else 1.5) * rc[:, 0].sum()
 
 
-@pytest.mark.parametrize("hash_bits", [7, 8, 9])
-def test_forgetful_visited_table_is_exact(svf, c1, hash_bits):
+@pytest.mark.parametrize("hash_bits,wpq", [(7, 1), (8, 1), (9, 1), (7, 2), (8, 2)])
+def test_forgetful_visited_table_is_exact(svf, c1, hash_bits, wpq):
     """Reading I7: clearing the table and re-registering the pool leaves results unchanged (tiny tables)."""
     X, Q, g, e = c1
     idx = svf.Index.from_state(X, g, e)
+    idx.set_warps_per_query(wpq)
     idx.set_search_params(1, 0, 0, hash_bits)
     ids, d = idx.search(cuda(Q), 10, 32)
     ri, rd, rc = oracle.graph_search(X, g, Q, 10, 32)
@@ -88,6 +92,7 @@ def test_search_with_tombstones_and_caps(svf, c1):
     dead = random_tombstones(len(X), 0.2, seed=7)
     tomb = pack_tomb(dead, len(X))
     idx = svf.Index.from_state(X, g, e, tomb=tomb)
+    idx.set_warps_per_query(2)
     assert idx.info()["n_deleted"] == len(dead)
     ids, d = idx.search(cuda(Q), 10, 64)
     ri, rd, _ = oracle.graph_search(X, g, Q, 10, 64, tomb=tomb)
@@ -99,13 +104,14 @@ def test_search_with_tombstones_and_caps(svf, c1):
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
 
 
-@pytest.mark.parametrize("dim,metric", [(128, 1), (96, 0), (200, 1), (13, 0), (3, 0)])
-def test_search_dims_and_metrics_integer(svf, dim, metric):
-    """Team sizes / padding (D not a multiple of 4) / inner product, ragged query count."""
+@pytest.mark.parametrize("dim,metric,wpq", [(128, 1, 1), (96, 0, 2), (200, 1, 2), (13, 0, 1), (3, 0, 2)])
+def test_search_dims_and_metrics_integer(svf, dim, metric, wpq):
+    """Team sizes / padding (D not a multiple of 4) / inner product, ragged query count, 1 or 2 warps per query."""
     X = int_rows(3000, dim, seed=dim, lo=-8 if metric else 0, hi=9 if metric else 64)
     Q = int_rows(77, dim, seed=dim + 1, lo=-8 if metric else 0, hi=9 if metric else 64)
-    g = random_graph(3000, 24, seed=dim)
+    g = random_graph(3000, 48, seed=dim)
     idx = svf.Index.from_state(X, g, metric=metric)
+    idx.set_warps_per_query(wpq)
     ids, d = idx.search(cuda(Q), 10, 64)
     ri, rd, _ = oracle.graph_search(X, g, Q, 10, 64, metric=metric)
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)

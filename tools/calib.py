@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--widths", default="1")
     ap.add_argument("--Ls", default="10,16,24,32,48,64,96,128")
     ap.add_argument("--hbits", default="0")
+    ap.add_argument("--wpq", default="0")
     a = ap.parse_args()
     c = config_spec(a.config)
     n = a.n or c["n"]
@@ -45,8 +46,10 @@ def main():
     print(f"knn_exact {nq} in {time.time() - t:.3f}s", flush=True)
     gt = gt.cpu().numpy()
     res = []
-    for w, hb in [(int(x), int(h)) for x in a.widths.split(",") for h in a.hbits.split(",")]:
+    for w, hb, wq in [(int(x), int(h), int(q)) for x in a.widths.split(",") for h in a.hbits.split(",")
+                      for q in a.wpq.split(",")]:
         idx.set_search_params(w, 0, 0, hb)
+        idx.set_warps_per_query(wq)
         for L in [int(x) for x in a.Ls.split(",")]:
             for _ in range(2):
                 ids, d = idx.search(Qd, 10, L)
@@ -63,7 +66,7 @@ def main():
             ids = ids.cpu().numpy()
             rec = np.mean([len(set(ids[i]) & set(gt[i])) / 10 for i in range(nq)])
             cnt = idx.last_search_counters()
-            r = dict(width=w, hbits=hb, L=L, recall=round(float(rec), 4), ms=round(ms, 3), qps=round(nq / ms * 1e3),
+            r = dict(width=w, hbits=hb, wpq=wq, L=L, recall=round(float(rec), 4), ms=round(ms, 3), qps=round(nq / ms * 1e3),
                      n_dist=cnt["n_dist"] / nq, iters=cnt["iters"] / nq)
             gbs = nq * (r["n_dist"] * c["dim"] * 4 + r["iters"] * w * c["degree"] * 4) / (ms * 1e-3) / 1e9
             r["alg_GBps"] = round(gbs, 1)
