@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-insert", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no GT / sweep / baselines")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
+    ap.add_argument("--wpq", type=int, default=0, help="warps per query (0 = auto)")
     return ap.parse_args()
 
 
@@ -178,6 +179,7 @@ def run_svf(a):
     t_build = time.time() - t0
     del Xd
     idx.set_search_params(a.search_width, 0, 0, a.hash_bits)
+    idx.set_warps_per_query(a.wpq)
     from paper_2601_08528_b200.sharded import ShardedIndex
 
     sh = ShardedIndex(idx, D.rank, D.world)          # global id g = local * G + r
