@@ -127,6 +127,7 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.cpl = MP / 32;
   int minbits = 1;
   while ((1 << minbits) < 4 * std::max(LP, MP)) ++minbits;  // forgetful-table invariant (I7)
+  while ((1 << minbits) < idx->Dp) ++minbits;                  // the table also stages the query row
   // default: small tables buy occupancy (the search is latency-bound); forgetting costs ~10% extra distances
   // at small L (measured: C2 L=14, 1024 slots 9.9M QPS vs 2048 slots 9.5M vs 4096 slots 7.3M)
   const int autobits = L <= 16 ? 10 : (L <= 48 ? 11 : (L <= 128 ? 12 : 13));

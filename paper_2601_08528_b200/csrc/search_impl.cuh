@@ -224,19 +224,19 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
     if (qi >= (unsigned long long)a.nq) break;
 
     // S0: the query fragment this lane needs (zero-padded to Dp), straight from global memory; clear the table
+    // the query is staged (coalesced) through the visited table, which is cleared right after (H >= Dp: host)
     const float* qg = a.Q + (size_t)qi * a.q_stride;
+    float* qstage = reinterpret_cast<float*>(tab);
+    for (int i = h * 32 + lane; i < a.dq * 4; i += 32 * WPQ) qstage[i] = i < a.q_dim ? __ldg(qg + i) : 0.f;
+    qsync<WPQ>(slot);
     float4 qv[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int c = tl + T * v;
-      float f[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = c * 4 + j;
-        f[j] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq && i < a.q_dim) ? __ldg(qg + i) : 0.f;
-      }
-      qv[v] = make_float4(f[0], f[1], f[2], f[3]);
+      qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? reinterpret_cast<const float4*>(qstage)[c]
+                                                               : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    qsync<WPQ>(slot);
     for (int i = h * 32 + lane; i < H; i += 32 * WPQ) tab[i] = kHashEmpty;
     qsync<WPQ>(slot);
     uint64_t pool[KPL];
@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
         running += __popc(m);
       }
       // S5: distances of this warp's survivors; S6: exchange + merge
+      if (WPQ == 1 && running == 0) continue;
       const int S2 = score_own<KPL, CPL, DQT>(a, pool, sid, keys_of(h, par), running, qv, lane);
       exchange_merge(running, S2);
     }
