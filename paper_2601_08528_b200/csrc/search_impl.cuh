@@ -429,6 +429,10 @@ static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   } else {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // the gathers are streaming (L1 hit rate ~0): give the unified L1/shared array to shared memory so the
+    // per-query visited tables never cap residency
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
     if (e != cudaSuccess) return e;
     cached_smem = smem;
