@@ -206,10 +206,10 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_d = out_d;
   a.counters = counters;
   a.work_counter = idx->small;
-  // pair mode (2 warps per query) halves per-query latency; worth it while the batch does not oversubscribe
-  // the resident warps many times (auto: nq below ~6 queries per resident warp slot)
+  // pair mode (2 warps per query) is exact but measured slower on C2 at every batch size tried (10K: 1.20 vs
+  // 0.85 ms; 40K: 4.2 vs 2.5 ms): the per-iteration pair barrier couples the warps and the merge is duplicated.
+  // Automatic = 1 warp per query.
   a.wpq = c.wpq;
-  if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && nq <= 6LL * idx->num_sms * 24) ? 2 : 1;
   cudaError_t e = cudaMemsetAsync(idx->small, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   cudaEvent_t pa;

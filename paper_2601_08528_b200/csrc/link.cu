@@ -67,19 +67,21 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     mpos[h] = (uint16_t)i;
   }
   __syncwarp();
-  // detour counts over the snapshot rows of C[0..m-1]
+  // detour counts over the snapshot rows of C[0..m-1]: 16 coalesced row slices in flight per lane
   const int total = m * R;
-  for (int f0 = 0; f0 < total; f0 += 32 * 4) {
-    uint32_t u[4];
-    int jj[4];
+  const int rshift = (R & (R - 1)) == 0 ? __ffs(R) - 1 : -1;
+  constexpr int UF = 16;
+  for (int f0 = 0; f0 < total; f0 += 32 * UF) {
+    uint32_t u[UF];
+    int jj[UF];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < UF; ++t) {
       const int f = f0 + t * 32 + lane;
-      jj[t] = f / R;
+      jj[t] = rshift >= 0 ? (f >> rshift) : f / R;
       u[t] = f < total ? __ldg(graph + (size_t)sC[jj[t]] * R + (f - jj[t] * R)) : kSent;
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < UF; ++t) {
       if (u[t] != kSent) {
         const int i = map_find(mid, mpos, mbits, u[t]);
         if (i > jj[t]) atomicAdd(cnt + i, 1u);
@@ -139,24 +141,25 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
 }
 
 // Reverse requests (u, key(d, v)) for every forward edge v -> u of the sub-batch.
+// (empty slots get the key `none`, the largest value the sort's bit range holds; all targets are < first < none)
 __global__ void reverse_emit_kernel(const uint32_t* __restrict__ graph, const float* __restrict__ edge_dist, int R,
-                                    int64_t first, int64_t n_new, uint32_t* __restrict__ ku,
+                                    int64_t first, int64_t n_new, uint32_t none, uint32_t* __restrict__ ku,
                                     uint64_t* __restrict__ kv) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_new * R) return;
   const int64_t b = t / R;
   const uint32_t v = (uint32_t)(first + b);
   const uint32_t u = graph[(size_t)v * R + (t - b * R)];
-  ku[t] = u;
+  ku[t] = u == kSent ? none : u;
   kv[t] = u == kSent ? kEmptyKey : make_key(edge_dist[(size_t)v * R + (t - b * R)], v);
 }
 
-__global__ void segment_heads_kernel(const uint32_t* __restrict__ ku, int64_t n, uint32_t* __restrict__ heads,
-                                     unsigned int* __restrict__ nseg) {
+__global__ void segment_heads_kernel(const uint32_t* __restrict__ ku, int64_t n, uint32_t none,
+                                     uint32_t* __restrict__ heads, unsigned int* __restrict__ nseg) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t u = ku[i];
-  if (u != kSent && (i == 0 || ku[i - 1] != u)) heads[atomicAdd(nseg, 1u)] = (uint32_t)i;
+  if (u != none && (i == 0 || ku[i - 1] != u)) heads[atomicAdd(nseg, 1u)] = (uint32_t)i;
 }
 
 // One warp per target u: tail(u) <- first (R-P) of sort_eff(tail(u) U requests(u)); prefix untouched; rows of
@@ -291,12 +294,15 @@ cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* to
   size_t temp = cub_temp_bytes(m);
   if ((size_t)(p - static_cast<unsigned char*>(scratch)) + temp > scratch_bytes) return cudaErrorInvalidValue;
   const unsigned blocks = (unsigned)((m + 255) / 256);
-  reverse_emit_kernel<<<blocks, 256, 0, st>>>(graph, edge_dist, R, first, n_new, ku, kv);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(p, temp, ku, ku2, kv, kv2, (int)m, 0, 32, st);
+  int bits = 1;
+  while (bits < 32 && ((int64_t)1 << bits) <= first) ++bits;  // 2^bits > first: every target id fits
+  const uint32_t none = bits >= 32 ? 0xFFFFFFFFu : (uint32_t)(((uint64_t)1 << bits) - 1);
+  reverse_emit_kernel<<<blocks, 256, 0, st>>>(graph, edge_dist, R, first, n_new, none, ku, kv);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(p, temp, ku, ku2, kv, kv2, (int)m, 0, bits, st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(nseg, 0, 4, st);
   if (e != cudaSuccess) return e;
-  segment_heads_kernel<<<blocks, 256, 0, st>>>(ku2, m, heads, nseg);
+  segment_heads_kernel<<<blocks, 256, 0, st>>>(ku2, m, none, heads, nseg);
   const unsigned ablocks = (unsigned)std::min<int64_t>((m + kLinkWarps - 1) / kLinkWarps, 148 * 16);
   reverse_apply_kernel<<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
   return cudaGetLastError();
