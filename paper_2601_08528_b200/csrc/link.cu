@@ -35,9 +35,10 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int M = 1 << mbits;
-  const size_t per_warp = (size_t)nc * 4 + (size_t)nc * 4 + (size_t)M * 4 + (size_t)M * 2 + 16;
+  const size_t per_warp = (size_t)nc * 4 + (size_t)nc * 4 + (size_t)M * 4 + (size_t)M * 2 + 16 + 512;
   unsigned char* base = smem + ((per_warp + 15) & ~(size_t)15) * wib;
-  uint32_t* sC = reinterpret_cast<uint32_t*>(base);
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(base);  // 4096-bit membership filter of C (quick reject)
+  uint32_t* sC = bloom + 128;
   uint32_t* cnt = sC + nc;
   uint32_t* mid = cnt + nc;
   uint16_t* mpos = reinterpret_cast<uint16_t*>(mid + M);
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
   const float* Cd = cand_d + b * nc;
 
   for (int i = lane; i < M; i += 32) mid[i] = kSent;
+  for (int i = lane; i < 128; i += 32) bloom[i] = 0u;
   int m = nc;
   for (int i0 = 0; i0 < nc; i0 += 32) {
     const int i = i0 + lane;
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     uint32_t h = (c * 0x9E3779B1u) >> (32 - mbits);
     while (atomicCAS(mid + h, kSent, c) != kSent) h = (h + 1) & (uint32_t)(M - 1);
     mpos[h] = (uint16_t)i;
+    const uint32_t fb = (c * 0x85EBCA6Bu) >> 20;
+    atomicOr(bloom + (fb >> 5), 1u << (fb & 31));
   }
   __syncwarp();
   // detour counts over the snapshot rows of C[0..m-1]: 16 coalesced row slices in flight per lane
@@ -82,7 +86,8 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     }
 #pragma unroll
     for (int t = 0; t < UF; ++t) {
-      if (u[t] != kSent) {
+      const uint32_t fb = (u[t] * 0x85EBCA6Bu) >> 20;
+      if (u[t] != kSent && ((bloom[fb >> 5] >> (fb & 31)) & 1u)) {
         const int i = map_find(mid, mpos, mbits, u[t]);
         if (i > jj[t]) atomicAdd(cnt + i, 1u);
       }
@@ -164,13 +169,15 @@ __global__ void segment_heads_kernel(const uint32_t* __restrict__ ku, int64_t n,
 
 // One warp per target u: tail(u) <- first (R-P) of sort_eff(tail(u) U requests(u)); prefix untouched; rows of
 // deleted u are frozen.  Tombstoned / empty tail entries count as +inf but keep their stored distance.
+// ET = registers per lane for the tail (R-P <= 32*ET); requests arrive in 32-wide chunks (typically 1-3 per target).
+template <int ET>
 __global__ void __launch_bounds__(kLinkWarps * 32)
     reverse_apply_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist,
                          const uint32_t* __restrict__ tomb, int R, int P, const uint32_t* __restrict__ ku,
                          const uint64_t* __restrict__ kv, int64_t n, const uint32_t* __restrict__ heads,
                          const unsigned int* __restrict__ nseg) {
-  __shared__ uint32_t old_id[kLinkWarps][128];
-  __shared__ float old_d[kLinkWarps][128];
+  __shared__ uint32_t old_id[kLinkWarps][32 * ET];
+  __shared__ float old_d[kLinkWarps][32 * ET];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const unsigned int S = *nseg;
   const int TS = R - P;
@@ -189,9 +196,10 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
       end += __ffs(~same) - 1;
       break;
     }
-    uint64_t best[4];
+    uint64_t best[ET];
+    bool sorted = true;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < ET; ++r) {
       const int e = r * 32 + lane;
       best[r] = kEmptyKey;
       if (e < TS) {
@@ -202,27 +210,31 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
         if (id != kSent) best[r] = make_key(tomb_dead(tomb, id) ? __int_as_float(0x7F800000) : d, id);
       }
     }
-    __syncwarp();
-    warp_sort<4>(best, lane);
-    for (int64_t c0 = start; c0 < end; c0 += 128) {
-      uint64_t cand[4];
+    // the tail is kept sorted; it only goes out of order when an entry was tombstoned since (then re-sort)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t i = c0 + r * 32 + lane;
-        cand[r] = i < end ? kv[i] : kEmptyKey;
-      }
-      warp_sort<4>(cand, lane);
-      warp_merge_into<4, 4>(best, cand, lane);
+    for (int r = 0; r < ET; ++r) {
+      uint64_t nx = __shfl_down_sync(0xffffffffu, best[r], 1);
+      const uint64_t head_next = __shfl_sync(0xffffffffu, best[r + 1 < ET ? r + 1 : r], 0);
+      if (lane == 31) nx = r + 1 < ET ? head_next : kEmptyKey;
+      sorted = sorted && best[r] <= nx;
+    }
+    if (!__all_sync(0xffffffffu, sorted)) warp_sort<ET>(best, lane);
+    __syncwarp();
+    for (int64_t c0 = start; c0 < end; c0 += 32) {
+      uint64_t cand[1];
+      cand[0] = c0 + lane < end ? kv[c0 + lane] : kEmptyKey;
+      warp_sort<1>(cand, lane);
+      warp_merge_into<ET, 1>(best, cand, lane);
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < ET; ++r) {
       const int e = r * 32 + lane;
       if (e < TS) {
         const uint32_t id = key_id(best[r]);
         float d = key_dist(best[r]);
         if (id != kSent && __float_as_uint(d) == 0x7F800000u) {  // a tombstoned old entry: keep its distance
-          for (int s = 0; s < TS; ++s)
-            if (old_id[wib][s] == id) d = old_d[wib][s];
+          for (int s2 = 0; s2 < TS; ++s2)
+            if (old_id[wib][s2] == id) d = old_d[wib][s2];
         }
         graph[(size_t)u * R + P + e] = id;
         edge_dist[(size_t)u * R + P + e] = d;
@@ -238,7 +250,7 @@ cudaError_t launch_detour_e(uint32_t* graph, float* edge_dist, int R, int P, int
   int mbits = 1;
   while ((1 << mbits) < 2 * nc || (1 << mbits) < 256) ++mbits;  // >= 2x load factor, room for 128 tail keys
   const int M = 1 << mbits;
-  const size_t per_warp = (((size_t)nc * 8 + (size_t)M * 6 + 16) + 15) & ~(size_t)15;
+  const size_t per_warp = (((size_t)nc * 8 + (size_t)M * 6 + 16 + 512) + 15) & ~(size_t)15;
   const size_t smem = per_warp * kLinkWarps;
   auto kern = detour_select_kernel<E>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -304,7 +316,13 @@ cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* to
   if (e != cudaSuccess) return e;
   segment_heads_kernel<<<blocks, 256, 0, st>>>(ku2, m, none, heads, nseg);
   const unsigned ablocks = (unsigned)std::min<int64_t>((m + kLinkWarps - 1) / kLinkWarps, 148 * 16);
-  reverse_apply_kernel<<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
+  const int TS = R - P;
+  if (TS <= 32)
+    reverse_apply_kernel<1><<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
+  else if (TS <= 64)
+    reverse_apply_kernel<2><<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
+  else
+    reverse_apply_kernel<4><<<ablocks, kLinkWarps * 32, 0, st>>>(graph, edge_dist, tomb, R, P, ku2, kv2, m, heads, nseg);
   return cudaGetLastError();
 }
 
