@@ -397,6 +397,63 @@ int orc_build(const float* X, int64_t n, int D, int metric, int R, int P, int L_
   return 0;
 }
 
+// NEXT-1: localized topology-aware repair, reading R1 in DESIGN.md:
+//   V^L = live v < n_alloc whose non-sentinel row entries are more than `threshold` deleted (strict);
+//   for each v in V^L, for each deleted p in row(v) in slot order, take the first c members of N_out(p) in slot
+//   order that are live, != v, not a live entry of row(v) and not already taken ("at most c vertices from
+//   N_out(p)"); new row = the R nearest of (live entries, stored distances) U (candidates, fresh
+//   distances) by (dist, id), sorted, i.e. prefix = the P nearest and tail = the rest (a seed row's layout).
+// All rows are read from the state at the start of the call (rows of deleted p are frozen; only V^L rows change).
+// hist[5] counts live rows by deleted fraction: 0, (0,0.1), [0.1,0.4], (0.4,threshold], >threshold (Fig. 5).
+int orc_repair(const float* X, int D, int metric, uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R,
+               int64_t n_alloc, int c, double threshold, int64_t* n_repaired, int64_t* hist) {
+  std::vector<uint32_t> snap(graph, graph + (size_t)n_alloc * R);
+  std::vector<float> snapd(edge_dist, edge_dist + (size_t)n_alloc * R);
+  int64_t repaired = 0;
+  for (int i = 0; i < 5; ++i) hist[i] = 0;
+  for (int64_t v = 0; v < n_alloc; ++v) {
+    if (dead(tomb, (uint32_t)v)) continue;
+    const uint32_t* row = snap.data() + (size_t)v * R;
+    int total = 0, ndead = 0;
+    for (int s = 0; s < R; ++s)
+      if (row[s] != SENT) {
+        total++;
+        if (dead(tomb, row[s])) ndead++;
+      }
+    const double frac = total ? (double)ndead / total : 0.0;
+    int bucket = ndead == 0 ? 0 : (frac < 0.1 ? 1 : (frac <= 0.4 ? 2 : (frac <= threshold ? 3 : 4)));
+    hist[bucket]++;
+    if (!(frac > threshold)) continue;
+    std::vector<Entry> pool;
+    std::unordered_set<uint32_t> taken;
+    for (int s = 0; s < R; ++s)
+      if (row[s] != SENT && !dead(tomb, row[s])) {
+        pool.push_back({snapd[(size_t)v * R + s], row[s], false});
+        taken.insert(row[s]);
+      }
+    for (int s = 0; s < R; ++s) {
+      const uint32_t p = row[s];
+      if (p == SENT || !dead(tomb, p)) continue;
+      int got = 0;
+      for (int t = 0; t < R && got < c; ++t) {
+        const uint32_t x = snap[(size_t)p * R + t];
+        if (x == SENT || dead(tomb, x) || x == (uint32_t)v || taken.count(x)) continue;
+        taken.insert(x);
+        pool.push_back({dist(X + (size_t)v * D, X + (size_t)x * D, D, metric), x, false});
+        got++;
+      }
+    }
+    std::sort(pool.begin(), pool.end(), key_less);
+    for (int s = 0; s < R; ++s) {
+      graph[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].id : SENT;
+      edge_dist[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].d : INF;
+    }
+    repaired++;
+  }
+  *n_repaired = repaired;
+  return 0;
+}
+
 // O6: merge of per-shard top-k lists (global ids) into the first k by key.
 int orc_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids, float* out_d) {
   for (int64_t q = 0; q < nq; ++q) {

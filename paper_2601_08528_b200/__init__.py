@@ -144,6 +144,13 @@ class Index:
         check(lib().svf_delete(self._h, ptr, n, ctypes.byref(newly), _stream(dev)))
         return newly.value
 
+    def repair(self, c: int = 8, threshold: float = 0.5) -> dict:
+        """Localized topology-aware repair of severely affected vertices (svf_repair)."""
+        n = ctypes.c_int64()
+        hist = (ctypes.c_uint64 * 5)()
+        check(lib().svf_repair(self._h, c, threshold, ctypes.byref(n), hist, None))
+        return {"repaired": n.value, "hist": list(hist)}
+
     def knn_exact(self, Q, k: int):
         """Exact k-NN over the live set (svf_knn_exact; ground truth)."""
         qp, qk, dev = _prep(Q, np.float32, torch.float32 if torch else None)

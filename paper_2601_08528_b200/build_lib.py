@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsvf.so")
 SOURCES = ["index.cu", "search.cu", "search_d0.cu", "search_d24.cu", "search_d32.cu", "search_d50.cu", "link.cu",
-           "knn.cu", "knn_tc.cu"]
+           "knn.cu", "knn_tc.cu", "repair.cu"]
 HEADERS = ["common.cuh", "kernels.h", "search_impl.cuh", os.path.join("..", "..", "include", "svf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

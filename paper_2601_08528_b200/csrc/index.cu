@@ -699,6 +699,29 @@ svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
   return SVF_OK;
 }
 
+svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
+                      void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (c < 1 || c > 32 || !(threshold >= 0.0 && threshold < 1.0))
+    return fail(SVF_ERR_INVALID, "need 1 <= c <= 32 and 0 <= threshold < 1");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(idx, ensure_scratch(idx, repair_scratch_bytes(idx->n_alloc), st), "repair scratch");
+  int64_t nr = 0;
+  uint64_t h[5];
+  CK(idx,
+     launch_repair(idx->graph, idx->edge_dist, idx->vec, idx->dq, idx->p.metric,
+                   idx->n_deleted > 0 ? idx->tomb : nullptr, idx->R, idx->n_alloc, c, threshold, idx->scratch,
+                   idx->scratch_bytes, idx->num_sms, st, &nr, h),
+     "repair");
+  if (n_repaired) *n_repaired = nr;
+  if (hist)
+    for (int i = 0; i < 5; ++i) hist[i] = h[i];
+  return SVF_OK;
+}
+
 svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq) {
   svf_status s = enter(idx);
   if (s != SVF_OK) return s;

@@ -72,6 +72,13 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
 cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
                               float* out_d, cudaStream_t st);
 
+// NEXT-1 localized repair (repair.cu)
+size_t repair_scratch_bytes(int64_t n_alloc);
+cudaError_t launch_repair(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                          const uint32_t* tomb, int R, int64_t n_alloc, int c, double threshold, void* scratch,
+                          size_t scratch_bytes, int num_sms, cudaStream_t st, int64_t* n_repaired,
+                          uint64_t hist_out[5]);
+
 // small helpers
 cudaError_t launch_pad_rows(const float* src, int64_t n, int dim, float* dst, int dq, cudaStream_t st);
 cudaError_t launch_fill_rows(uint32_t* graph, float* edge_dist, int64_t first, int64_t n, int R, cudaStream_t st);

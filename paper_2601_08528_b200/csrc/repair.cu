@@ -1,0 +1,207 @@
+// NEXT-1: localized topology-aware repair of severely affected vertices, reading R1
+// in DESIGN.md.  Two kernels over the state at the start of the call (rows of deleted vertices are frozen and only
+// rows of V^L are rewritten, so every row is read unmodified):
+//   repair_mark_kernel   warp per row: deleted fraction of the non-sentinel entries, histogram of Fig. 5 buckets,
+//                        append v to V^L when the fraction exceeds the threshold (strict);
+//   repair_apply_kernel  warp per v in V^L: for each deleted p in row(v) in slot order take the first c members of
+//                        N_out(p) in slot order that are live, != v, not a live entry of row(v) and not yet taken;
+//                        new row = the R nearest of (live entries with their stored distances, candidates with
+//                        fresh FFMA distances) by (dist, id), sorted (prefix = the P nearest, tail = the rest).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svf {
+
+namespace {
+
+constexpr int kRepWarps = 4;
+
+__global__ void repair_mark_kernel(const uint32_t* __restrict__ graph, const uint32_t* __restrict__ tomb, int R,
+                                   int64_t n_alloc, double threshold, uint32_t* __restrict__ list,
+                                   unsigned int* __restrict__ n_list, unsigned long long* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (v >= n_alloc || tomb_dead(tomb, (uint32_t)v)) return;
+  int total = 0, ndead = 0;
+  for (int s = lane; s < R; s += 32) {
+    const uint32_t x = graph[(size_t)v * R + s];
+    if (x != kSent) {
+      ++total;
+      if (tomb_dead(tomb, x)) ++ndead;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    total += __shfl_xor_sync(0xffffffffu, total, off);
+    ndead += __shfl_xor_sync(0xffffffffu, ndead, off);
+  }
+  if (lane == 0) {
+    const double frac = total ? (double)ndead / (double)total : 0.0;
+    const int bucket = ndead == 0 ? 0 : (frac < 0.1 ? 1 : (frac <= 0.4 ? 2 : (frac <= threshold ? 3 : 4)));
+    atomicAdd(hist + bucket, 1ull);
+    if (frac > threshold) list[atomicAdd(n_list, 1u)] = (uint32_t)v;
+  }
+}
+
+__device__ __forceinline__ bool set_has(const uint32_t* tab, int bits, uint32_t id) {
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t h = (id * 0x9E3779B1u) >> (32 - bits);
+  for (;;) {
+    const uint32_t x = tab[h];
+    if (x == id) return true;
+    if (x == kSent) return false;
+    h = (h + 1) & mask;
+  }
+}
+__device__ __forceinline__ void set_put(uint32_t* tab, int bits, uint32_t id) {
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t h = (id * 0x9E3779B1u) >> (32 - bits);
+  while (atomicCAS(tab + h, kSent, id) != kSent && tab[h] != id) h = (h + 1) & mask;
+}
+
+// ER = registers per lane for a row (R <= 32*ER)
+template <int ER>
+__global__ void __launch_bounds__(kRepWarps * 32)
+    repair_apply_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist, const float* __restrict__ vec,
+                        int dq, int metric, const uint32_t* __restrict__ tomb, int R, int c,
+                        const uint32_t* __restrict__ list, const unsigned int* __restrict__ n_list, int set_bits,
+                        int cand_cap) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)cand_cap * 4 + (size_t)cand_cap * 8 + 15) & ~(size_t)15;
+  unsigned char* base = smem + per_warp * wib;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(base);
+  uint32_t* cid = tab + (1 << set_bits);
+  uint64_t* ckey = reinterpret_cast<uint64_t*>(cid + cand_cap);
+  const unsigned int nv = *n_list;
+  for (unsigned int w = blockIdx.x * kRepWarps + wib; w < nv; w += gridDim.x * kRepWarps) {
+    const uint32_t v = list[w];
+    for (int i = lane; i < (1 << set_bits); i += 32) tab[i] = kSent;
+    __syncwarp();
+    uint32_t rid[ER];
+    uint64_t best[ER];
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      rid[r] = s < R ? graph[(size_t)v * R + s] : kSent;
+      const bool live = rid[r] != kSent && !tomb_dead(tomb, rid[r]);
+      best[r] = live ? make_key(edge_dist[(size_t)v * R + s], rid[r]) : kEmptyKey;
+      if (live) set_put(tab, set_bits, rid[r]);
+    }
+    __syncwarp();
+    // candidates: deleted p in slot order, first c qualifying members of N_out(p) in slot order
+    int ncand = 0;
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t p = __shfl_sync(0xffffffffu, rid[r], l);
+        if (r * 32 + l >= R || p == kSent || !tomb_dead(tomb, p)) continue;
+        int got = 0;
+#pragma unroll
+        for (int r2 = 0; r2 < ER; ++r2) {
+          const int t = r2 * 32 + lane;
+          const uint32_t x = t < R ? graph[(size_t)p * R + t] : kSent;
+          const bool ok = x != kSent && x != v && !tomb_dead(tomb, x) && !set_has(tab, set_bits, x);
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          const int rank = got + __popc(m & ((1u << lane) - 1u));
+          const bool take = ok && rank < c && ncand + rank < cand_cap;
+          if (take) {
+            cid[ncand + rank] = x;
+            set_put(tab, set_bits, x);
+          }
+          got = min(got + __popc(m), c);
+        }
+        ncand = min(ncand + got, cand_cap);
+        __syncwarp();
+      }
+    }
+    // fresh distances of the candidates to v (a lane per candidate, rows read as float4)
+    const float4* xv = reinterpret_cast<const float4*>(vec) + (size_t)v * dq;
+    for (int i = lane; i < ncand; i += 32) {
+      const float4* xc = reinterpret_cast<const float4*>(vec) + (size_t)cid[i] * dq;
+      float acc = 0.f;
+      for (int j = 0; j < dq; ++j) {
+        const float4 a = __ldg(xv + j), b = __ldg(xc + j);
+        if (metric == 0) {
+          const float d0 = b.x - a.x, d1 = b.y - a.y, d2 = b.z - a.z, d3 = b.w - a.w;
+          acc = fmaf(d0, d0, acc);
+          acc = fmaf(d1, d1, acc);
+          acc = fmaf(d2, d2, acc);
+          acc = fmaf(d3, d3, acc);
+        } else {
+          acc = fmaf(b.x, a.x, acc);
+          acc = fmaf(b.y, a.y, acc);
+          acc = fmaf(b.z, a.z, acc);
+          acc = fmaf(b.w, a.w, acc);
+        }
+      }
+      ckey[i] = make_key((metric == 0 ? acc : -acc) + 0.0f, cid[i]);
+    }
+    __syncwarp();
+    warp_sort<ER>(best, lane);
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+      uint64_t cc[1];
+      cc[0] = c0 + lane < ncand ? ckey[c0 + lane] : kEmptyKey;
+      warp_sort<1>(cc, lane);
+      warp_merge_into<ER, 1>(best, cc, lane);
+    }
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      if (s < R) {
+        graph[(size_t)v * R + s] = key_id(best[r]);
+        edge_dist[(size_t)v * R + s] = key_dist(best[r]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+size_t repair_scratch_bytes(int64_t n_alloc) { return (size_t)n_alloc * 4 + 1024; }
+
+cudaError_t launch_repair(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                          const uint32_t* tomb, int R, int64_t n_alloc, int c, double threshold, void* scratch,
+                          size_t scratch_bytes, int num_sms, cudaStream_t st, int64_t* n_repaired,
+                          uint64_t hist_out[5]) {
+  if (n_alloc <= 0) {
+    *n_repaired = 0;
+    for (int i = 0; i < 5; ++i) hist_out[i] = 0;
+    return cudaSuccess;
+  }
+  if (scratch_bytes < repair_scratch_bytes(n_alloc)) return cudaErrorInvalidValue;
+  uint32_t* list = static_cast<uint32_t*>(scratch);
+  unsigned long long* hist =
+      reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + (((size_t)n_alloc * 4 + 255) & ~(size_t)255));
+  unsigned int* n_list = reinterpret_cast<unsigned int*>(hist + 5);
+  cudaError_t e = cudaMemsetAsync(hist, 0, 64, st);
+  if (e != cudaSuccess) return e;
+  repair_mark_kernel<<<(unsigned)((n_alloc + 7) / 8), 256, 0, st>>>(graph, tomb, R, n_alloc, threshold, list, n_list,
+                                                                    hist);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int cand_cap = c * R;
+  int set_bits = 1;
+  while ((1 << set_bits) < 2 * (R + cand_cap)) ++set_bits;
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)cand_cap * 12 + 15) & ~(size_t)15;
+  const size_t smem = per_warp * kRepWarps;
+  auto run = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<(unsigned)(num_sms * 8), kRepWarps * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, c, list,
+                                                                n_list, set_bits, cand_cap);
+    return cudaGetLastError();
+  };
+  if (R <= 32) e = run(repair_apply_kernel<1>);
+  else if (R <= 64) e = run(repair_apply_kernel<2>);
+  else e = run(repair_apply_kernel<4>);
+  if (e != cudaSuccess) return e;
+  unsigned long long hh[6];
+  if ((e = cudaMemcpyAsync(hh, hist, 48, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  for (int i = 0; i < 5; ++i) hist_out[i] = hh[i];
+  *n_repaired = (int64_t)(hh[5] & 0xFFFFFFFFull);
+  return cudaSuccess;
+}
+
+}  // namespace svf

@@ -288,3 +288,21 @@ def test_read_after_write(svf, c1):
     idx.insert(cuda(X[n0:]))
     ids, _ = idx.search(cuda(X[n0:]), 1, 32)
     assert np.mean(u32(ids)[:, 0] == np.arange(n0, len(X))) >= 0.95
+
+
+# ---- NEXT-1 localized repair ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("frac,c,thr", [(0.45, 8, 0.5), (0.3, 4, 0.3), (0.6, 8, 0.5)])
+def test_repair_bit_exact_integer_data(svf, c1, frac, c, thr):
+    X, Q, g, e = c1
+    dead = random_tombstones(len(X), frac, seed=int(frac * 100))
+    tomb = pack_tomb(dead, len(X))
+    gr, er, nrep, hist = oracle.repair(X, g, e, tomb, c=c, threshold=thr)
+    idx = svf.Index.from_state(X, g, e, tomb=tomb)
+    out = idx.repair(c=c, threshold=thr)
+    st = idx.export()
+    assert out["repaired"] == nrep and out["hist"] == hist.tolist()
+    assert np.array_equal(st["graph"], gr) and np.array_equal(st["edge_dist"], er)
+    # searches over the repaired graph still match the oracle bit-exactly
+    ids, d = idx.search(cuda(Q), 10, 32)
+    ri, rd, _ = oracle.graph_search(X, gr, Q, 10, 32, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)

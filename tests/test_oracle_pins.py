@@ -394,3 +394,57 @@ def test_shard_merge_identical_for_any_gpu_count(orc):
 def test_spec_recall_examples(orc):
     for res, gt, want in golden("spec_examples.json")["recall"]["cases"]:
         assert abs(orc.recall_ids([res], [gt], 3) - want) < 1e-12
+
+
+# ---- NEXT-1 localized repair ----------------------------------------------------------------------------------------
+def _repair_golden():
+    g = golden("spec_examples.json")["repair"]
+    X = np.array(g["points"], np.float32)[:, None]
+    R = g["R"]
+    G = np.array([[SENT if v is None else v for v in row] for row in g["rows"]], np.uint32)
+    E = np.full(G.shape, np.inf, np.float32)
+    for v in range(len(G)):
+        for s in range(R):
+            if G[v, s] != SENT:
+                E[v, s] = (X[v, 0] - X[G[v, s], 0]) ** 2
+    return g, X, G, E
+
+
+def test_spec_repair_example(orc):
+    g, X, G, E = _repair_golden()
+    tomb = pack_tomb(g["deleted"], len(X))
+    g2, e2, nrep, hist = orc.repair(X, G, E, tomb, c=g["c"], threshold=g["threshold"])
+    assert g2[0].tolist() == g["expect_row0"] and e2[0].tolist() == g["expect_d0"]
+    assert nrep == 1 and hist.sum() == len(X) - len(g["deleted"])
+    assert np.array_equal(g2[1:], G[1:])                         # only V^L rows change
+    # strict threshold: 1/3 deleted is not > 0.5 -> nothing repaired (S:L392-393 boundary)
+    g3, _, nrep3, _ = orc.repair(X, G, E, tomb, c=g["c"], threshold=0.5)
+    assert nrep3 == 0 and np.array_equal(g3, G)
+    # all of N_out(p) deleted -> no candidates from p; v keeps its live neighbours only
+    tomb_all = pack_tomb([1, 4, 5, 6], len(X))
+    g4, _, _, _ = orc.repair(X, G, E, tomb_all, c=2, threshold=0.3)
+    assert g4[0].tolist() == [2, 3, SENT, SENT]
+
+
+def test_repair_properties_on_a_built_graph(orc):
+    X = GLM(dim=16, ell=6, integer=True).rows(8, 8, 0, 3000)
+    R, c = 16, 8
+    G, E = orc.build(X, R=R, seed_size=500, B_ins=400, L_ins=48)
+    dead = random_tombstones(3000, 0.45, seed=9)
+    tomb = pack_tomb(dead, 3000)
+    deadset = set(dead.tolist())
+    g2, e2, nrep, hist = orc.repair(X, G, E, tomb, c=c, threshold=0.5)
+    assert hist.sum() == 3000 - len(dead) and hist[4] == nrep > 0
+    changed = np.flatnonzero(np.any(g2 != G, axis=1))
+    for v in changed:
+        old = [int(x) for x in G[v] if x != SENT]
+        assert sum(x in deadset for x in old) / len(old) > 0.5       # only severely affected vertices
+        new = [int(x) for x in g2[v] if x != SENT]
+        assert not (set(new) & deadset) and v not in new and len(set(new)) == len(new)
+        assert list(e2[v][: len(new)]) == sorted(e2[v][: len(new)])
+        allowed = set(x for x in old if x not in deadset)
+        per_p = {p: [int(x) for x in G[p] if x != SENT] for p in old if p in deadset}
+        for x in new:
+            if x not in allowed:
+                assert any(x in lst for lst in per_p.values())       # replacements come from N_out(p)
+        assert len(set(new) - allowed) <= c * len(per_p)            # O(cR) added edges
