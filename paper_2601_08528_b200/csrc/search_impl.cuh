@@ -72,7 +72,10 @@ struct Geo {
 template <int KPL, int CPL, int DQT>
 __device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
                                          uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
-  constexpr int U = 2;
+#ifndef SVF_GATHER_U
+#define SVF_GATHER_U 2
+#endif
+  constexpr int U = SVF_GATHER_U;  // vectors per team per round (U * 32/T vectors in flight per warp)
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
