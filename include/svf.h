@@ -134,8 +134,9 @@ svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* c
                                int64_t n_new, int32_t n_cand, void* stream);
 
 /* Warps serving one query in svf_search / svf_insert's search: 1, 2 (both warps keep identical pools and split the
- * candidate slots; used when degree * search_width > 32 and itopk <= 128), or 0 = automatic (currently 1: pair
- * mode measured slower on C2).  Results are identical for every setting. */
+ * candidate slots; used when degree * search_width > 32 and itopk <= 128: ~35% lower per-query latency, lower
+ * throughput once the batch fills the GPU), or 0 = automatic (2 while 2*nq <= 24 * SM count, else 1).  Results
+ * are identical for every setting (NEXT-2 low-latency path). */
 svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq);
 
 /* Exact-kNN engine: mode 0 = automatic (tcgen05 TF32 scoring + exact FFMA re-rank with a certificate, exact FFMA

@@ -136,7 +136,7 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
   c.n_init = n_init > 0 ? n_init : L;
-  c.wpq = idx->wpq == 2 ? 2 : 1;
+  c.wpq = idx->wpq == 2 ? 2 : 1;  // 0 (auto) is resolved per call from the batch size in run_search
   return true;
 }
 
@@ -206,10 +206,12 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_d = out_d;
   a.counters = counters;
   a.work_counter = idx->small;
-  // pair mode (2 warps per query) is exact but measured slower on C2 at every batch size tried (10K: 1.20 vs
-  // 0.85 ms; 40K: 4.2 vs 2.5 ms): the per-iteration pair barrier couples the warps and the merge is duplicated.
-  // Automatic = 1 warp per query.
+  // pair mode (2 warps per query, identical results) cuts per-query latency ~35% (C2 itopk 14: batch 1 p50
+  // 0.151 -> 0.091 ms, batch 1024 0.348 -> 0.239 ms; profiles/r01_latency_c2.json) but costs throughput once the
+  // batch fills the resident warps (4096: 0.51 vs 0.57 ms, 10K: 0.85 vs 1.20 ms).  Automatic: 2 while the batch
+  // needs at most half of the resident warp slots (~24 per SM), else 1.
   a.wpq = c.wpq;
+  if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
   cudaError_t e = cudaMemsetAsync(idx->small, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   cudaEvent_t pa;
