@@ -104,11 +104,11 @@ svf_status svf_delete(svf_index* idx, const uint32_t* ids, int64_t n, int64_t* n
 svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, uint32_t* out_ids,
                          float* out_dists, void* stream);
 
-/* Localized topology-aware repair (reading R1 in DESIGN.md): every live vertex whose
+/* Localized topology-aware repair (reading R1' in DESIGN.md): every live vertex whose
  * non-empty neighbour slots are more than `threshold` (paper: 0.5) deleted gets, for each deleted neighbour p (slot
  * order), the first c (paper: 8) live members of N_out(p) that are not itself and not already its neighbours;
- * its row becomes the R nearest of its live neighbours and those candidates, sorted by (distance, id).  Only those
- * rows change.  *n_repaired = rows rewritten; hist (nullable) = live rows by deleted-neighbour fraction in buckets
+ * its row is rebuilt by the insertion's selection rule (detour counts, protected prefix + sorted tail) over the
+ * insert_itopk nearest of its live neighbours and those candidates.  Only those rows change.  *n_repaired = rows rewritten; hist (nullable) = live rows by deleted-neighbour fraction in buckets
  * {0, (0,0.1), [0.1,0.4], (0.4,threshold], >threshold} (the distribution of Fig. 5).  Synchronous. */
 svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
                       void* stream);

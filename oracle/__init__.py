@@ -42,7 +42,8 @@ def lib():
         L.orc_insert.argtypes = [P, I, I, P, P, P, I, I, I64, I64, I, I, I, I, I, U64, I]
         L.orc_build.argtypes = [P, I64, I, I, I, I, I, I, I, I, I, I, U64, P, P, I]
         L.orc_merge_topk.argtypes = [P, P, I, I64, I, P, P]
-        L.orc_repair.argtypes = [P, I, I, P, P, P, I, I64, I, ctypes.c_double, P, P]
+        L.orc_repair.argtypes = [P, I, I, P, P, P, I, I, I64, I, ctypes.c_double, I, P, P]
+        L.orc_repair_mode.argtypes = [P, I, I, P, P, P, I, I, I64, I, ctypes.c_double, I, I, P, P]
         _lib = L
     return _lib
 
@@ -166,16 +167,19 @@ def build(X, R: int, P: Optional[int] = None, L_ins: int = 128, B_ins: int = 409
 
 
 def repair(X, graph, edge_dist, tomb, c: int = 8, threshold: float = 0.5, metric: int = 0,
-           n_alloc: Optional[int] = None):
-    """NEXT-1 localized repair on copies; returns (graph, edge_dist, n_repaired, hist[5])."""
+           n_alloc: Optional[int] = None, mode: int = 1, P: Optional[int] = None, cap: int = 128):
+    """NEXT-1 localized repair on copies; returns (graph, edge_dist, n_repaired, hist[5]).
+    mode 1 = reading R1' (insertion's detour selection over the union's `cap` nearest; the product's rule),
+    mode 0 = R1 (the R nearest of the union; experiment hook)."""
     X, tomb = _f32(X), _u32(tomb)
     graph = np.array(graph, dtype=np.uint32, copy=True, order="C")
     edge_dist = np.array(edge_dist, dtype=np.float32, copy=True, order="C")
     n_alloc = graph.shape[0] if n_alloc is None else n_alloc
+    R = graph.shape[1]
     nrep = ctypes.c_int64()
     hist = np.zeros(5, np.int64)
-    lib().orc_repair(_p(X), X.shape[1], metric, _p(graph), _p(edge_dist), _p(tomb), graph.shape[1], n_alloc, c,
-                     threshold, ctypes.byref(nrep), _p(hist))
+    lib().orc_repair_mode(_p(X), X.shape[1], metric, _p(graph), _p(edge_dist), _p(tomb), R,
+                          R // 2 if P is None else P, n_alloc, c, threshold, mode, cap, ctypes.byref(nrep), _p(hist))
     return graph, edge_dist, nrep.value, hist
 
 

@@ -397,16 +397,26 @@ int orc_build(const float* X, int64_t n, int D, int metric, int R, int P, int L_
   return 0;
 }
 
-// NEXT-1: localized topology-aware repair, reading R1 in DESIGN.md:
+// NEXT-1: localized topology-aware repair, reading R1' in DESIGN.md:
 //   V^L = live v < n_alloc whose non-sentinel row entries are more than `threshold` deleted (strict);
 //   for each v in V^L, for each deleted p in row(v) in slot order, take the first c members of N_out(p) in slot
 //   order that are live, != v, not a live entry of row(v) and not already taken ("at most c vertices from
-//   N_out(p)"); new row = the R nearest of (live entries, stored distances) U (candidates, fresh
-//   distances) by (dist, id), sorted, i.e. prefix = the P nearest and tail = the rest (a seed row's layout).
+//   N_out(p)"); U = (live entries, stored distances) U (candidates, fresh distances) sorted by (dist, id)
+//   and cut to its first `cap` (= insert_itopk); the new row is U's insertion selection (readings
+//   I10-I12: detour counts on the call's starting rows, prefix P in detour order, tail sorted by key).
+//   mode 0 (experiment hook, reading R1): the row is the R nearest of U instead.
 // All rows are read from the state at the start of the call (rows of deleted p are frozen; only V^L rows change).
 // hist[5] counts live rows by deleted fraction: 0, (0,0.1), [0.1,0.4], (0.4,threshold], >threshold (Fig. 5).
+int orc_repair_mode(const float* X, int D, int metric, uint32_t* graph, float* edge_dist, const uint32_t* tomb,
+                    int R, int P, int64_t n_alloc, int c, double threshold, int mode, int cap, int64_t* n_repaired,
+                    int64_t* hist);
 int orc_repair(const float* X, int D, int metric, uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R,
-               int64_t n_alloc, int c, double threshold, int64_t* n_repaired, int64_t* hist) {
+               int P, int64_t n_alloc, int c, double threshold, int cap, int64_t* n_repaired, int64_t* hist) {
+  return orc_repair_mode(X, D, metric, graph, edge_dist, tomb, R, P, n_alloc, c, threshold, 1, cap, n_repaired, hist);
+}
+int orc_repair_mode(const float* X, int D, int metric, uint32_t* graph, float* edge_dist, const uint32_t* tomb,
+                    int R, int P, int64_t n_alloc, int c, double threshold, int mode, int cap, int64_t* n_repaired,
+                    int64_t* hist) {
   std::vector<uint32_t> snap(graph, graph + (size_t)n_alloc * R);
   std::vector<float> snapd(edge_dist, edge_dist + (size_t)n_alloc * R);
   int64_t repaired = 0;
@@ -444,9 +454,21 @@ int orc_repair(const float* X, int D, int metric, uint32_t* graph, float* edge_d
       }
     }
     std::sort(pool.begin(), pool.end(), key_less);
-    for (int s = 0; s < R; ++s) {
-      graph[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].id : SENT;
-      edge_dist[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].d : INF;
+    if (mode == 1 && cap > 0 && (int)pool.size() > cap) pool.resize(cap);
+    if (mode == 1) {
+      std::vector<uint32_t> cid(pool.size());
+      std::vector<float> cd(pool.size());
+      for (size_t i = 0; i < pool.size(); ++i) {
+        cid[i] = pool[i].id;
+        cd[i] = pool[i].d;
+      }
+      forward_row(snap.data(), R, P, cid.data(), cd.data(), (int)pool.size(), graph + (size_t)v * R,
+                  edge_dist + (size_t)v * R);
+    } else {
+      for (int s = 0; s < R; ++s) {
+        graph[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].id : SENT;
+        edge_dist[(size_t)v * R + s] = s < (int)pool.size() ? pool[s].d : INF;
+      }
     }
     repaired++;
   }

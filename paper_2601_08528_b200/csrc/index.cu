@@ -710,15 +710,25 @@ svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_re
   std::lock_guard<std::mutex> lk(idx->mu);
   DeviceGuard g(idx->dev);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  CK(idx, ensure_scratch(idx, repair_scratch_bytes(idx->n_alloc), st), "repair scratch");
-  int64_t nr = 0;
+  const uint32_t* tomb = idx->n_deleted > 0 ? idx->tomb : nullptr;
+  CK(idx, ensure_scratch(idx, repair_mark_scratch_bytes(idx->n_alloc), st), "repair scratch");
+  int64_t n_list = 0;
   uint64_t h[5];
-  CK(idx,
-     launch_repair(idx->graph, idx->edge_dist, idx->vec, idx->dq, idx->p.metric,
-                   idx->n_deleted > 0 ? idx->tomb : nullptr, idx->R, idx->n_alloc, c, threshold, idx->scratch,
-                   idx->scratch_bytes, idx->num_sms, st, &nr, h),
-     "repair");
-  if (n_repaired) *n_repaired = nr;
+  CK(idx, launch_repair_mark(idx->graph, tomb, idx->R, idx->n_alloc, threshold, idx->scratch, st, &n_list, h),
+     "repair mark");
+  if (n_list > 0) {
+    const int cap = idx->p.insert_itopk;  // U is cut to an insertion-sized candidate list (reading R1')
+    const size_t bytes = repair_apply_scratch_bytes(n_list, idx->R, cap);
+    void* sp = nullptr;
+    CK(idx, cudaMallocAsync(&sp, bytes, st), "repair apply scratch");
+    CK(idx,
+       launch_repair_apply(idx->graph, idx->edge_dist, idx->vec, idx->dq, idx->p.metric, tomb, idx->R, idx->P, c, cap,
+                           idx->scratch, n_list, sp, bytes, idx->num_sms, st),
+       "repair apply");
+    CK(idx, cudaFreeAsync(sp, st), "repair free");
+    CK(idx, cudaStreamSynchronize(st), "repair sync");
+  }
+  if (n_repaired) *n_repaired = n_list;
   if (hist)
     for (int i = 0; i < 5; ++i) hist[i] = h[i];
   return SVF_OK;

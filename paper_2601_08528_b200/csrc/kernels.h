@@ -43,6 +43,9 @@ cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStrea
 // (reads the snapshot rows of the candidates, writes rows first..first+n_new-1; disjoint by construction)
 cudaError_t launch_detour_select(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
                                  const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st);
+// K-L1 into an arbitrary output buffer (row b -> out + b*R), counting detours on `graph` (used by repair)
+cudaError_t launch_detour_rows(const uint32_t* graph, uint32_t* out_ids, float* out_d, int R, int P, int64_t n,
+                               const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st);
 // K-L2: reverse edges.  Scratch must hold 2*n_new*R u32 + 2*n_new*R u64 + n_new*R u32 + cub temp bytes.
 size_t reverse_scratch_bytes(int64_t n_new, int R);
 cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R, int P, int64_t first,
@@ -73,11 +76,14 @@ cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_
                               float* out_d, cudaStream_t st);
 
 // NEXT-1 localized repair (repair.cu)
-size_t repair_scratch_bytes(int64_t n_alloc);
-cudaError_t launch_repair(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
-                          const uint32_t* tomb, int R, int64_t n_alloc, int c, double threshold, void* scratch,
-                          size_t scratch_bytes, int num_sms, cudaStream_t st, int64_t* n_repaired,
-                          uint64_t hist_out[5]);
+// phase 1: V^L list + histogram (returns |V^L| after a sync); phase 2: rewrite those rows (reading R1')
+size_t repair_mark_scratch_bytes(int64_t n_alloc);
+cudaError_t launch_repair_mark(const uint32_t* graph, const uint32_t* tomb, int R, int64_t n_alloc, double threshold,
+                               void* scratch, cudaStream_t st, int64_t* n_list, uint64_t hist_out[5]);
+size_t repair_apply_scratch_bytes(int64_t n_list, int R, int cap);
+cudaError_t launch_repair_apply(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                                const uint32_t* tomb, int R, int P, int c, int cap, const void* mark_scratch,
+                                int64_t n_list, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t st);
 
 // small helpers
 cudaError_t launch_pad_rows(const float* src, int64_t n, int dim, float* dst, int dq, cudaStream_t st);

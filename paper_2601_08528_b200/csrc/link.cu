@@ -27,11 +27,12 @@ __device__ __forceinline__ int map_find(const uint32_t* mid, const uint16_t* mpo
 // One warp per new vertex v = first + b.  Candidate list C = cand_ids[b][0..m) (distance order, SENT-padded).
 // count(i) = |{ j < i : C[i] in row(C[j]) }| ("detourable paths"); stable sort by (count, i) (I11);
 // select the first min(R, m): prefix [0,P) in detour order, tail [P,R) sorted by key(d, id) (I12).
+// Rows are read from `graph` (the snapshot) and written to out_ids/out_d row b (disjoint from every row read).
 template <int E>
 __global__ void __launch_bounds__(kLinkWarps * 32)
-    detour_select_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist, int R, int P, int64_t first,
-                         int64_t n_new, const uint32_t* __restrict__ cand_ids, const float* __restrict__ cand_d,
-                         int nc, int mbits) {
+    detour_select_kernel(const uint32_t* __restrict__ graph, uint32_t* __restrict__ out_ids,
+                         float* __restrict__ out_d, int R, int P, int64_t n_new,
+                         const uint32_t* __restrict__ cand_ids, const float* __restrict__ cand_d, int nc, int mbits) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int M = 1 << mbits;
@@ -103,8 +104,8 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
   warp_sort<E>(key, lane);  // (count, i) ascending == stable sort by count
   const int sel = min(R, m);
   const int npre = min(P, sel);
-  uint32_t* row = graph + (size_t)(first + b) * R;
-  float* rowd = edge_dist + (size_t)(first + b) * R;
+  uint32_t* row = out_ids + (size_t)b * R;
+  float* rowd = out_d + (size_t)b * R;
   for (int s = lane; s < R; s += 32) {
     row[s] = kSent;
     rowd[s] = __int_as_float(0x7F800000);
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
 }
 
 template <int E>
-cudaError_t launch_detour_e(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
+cudaError_t launch_detour_e(const uint32_t* graph, uint32_t* out_ids, float* out_d, int R, int P, int64_t n_new,
                             const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
   int mbits = 1;
   while ((1 << mbits) < 2 * nc || (1 << mbits) < 256) ++mbits;  // >= 2x load factor, room for 128 tail keys
@@ -256,21 +257,28 @@ cudaError_t launch_detour_e(uint32_t* graph, float* edge_dist, int R, int P, int
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)((n_new + kLinkWarps - 1) / kLinkWarps);
-  kern<<<blocks, kLinkWarps * 32, smem, st>>>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, mbits);
+  kern<<<blocks, kLinkWarps * 32, smem, st>>>(graph, out_ids, out_d, R, P, n_new, cand_ids, cand_d, nc, mbits);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+cudaError_t launch_detour_rows(const uint32_t* graph, uint32_t* out_ids, float* out_d, int R, int P, int64_t n,
+                               const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (nc <= 32) return launch_detour_e<1>(graph, out_ids, out_d, R, P, n, cand_ids, cand_d, nc, st);
+  if (nc <= 64) return launch_detour_e<2>(graph, out_ids, out_d, R, P, n, cand_ids, cand_d, nc, st);
+  if (nc <= 128) return launch_detour_e<4>(graph, out_ids, out_d, R, P, n, cand_ids, cand_d, nc, st);
+  if (nc <= 256) return launch_detour_e<8>(graph, out_ids, out_d, R, P, n, cand_ids, cand_d, nc, st);
+  if (nc <= 512) return launch_detour_e<16>(graph, out_ids, out_d, R, P, n, cand_ids, cand_d, nc, st);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_detour_select(uint32_t* graph, float* edge_dist, int R, int P, int64_t first, int64_t n_new,
                                  const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
-  if (n_new <= 0) return cudaSuccess;
-  if (nc <= 32) return launch_detour_e<1>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
-  if (nc <= 64) return launch_detour_e<2>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
-  if (nc <= 128) return launch_detour_e<4>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
-  if (nc <= 256) return launch_detour_e<8>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
-  if (nc <= 512) return launch_detour_e<16>(graph, edge_dist, R, P, first, n_new, cand_ids, cand_d, nc, st);
-  return cudaErrorInvalidValue;
+  // new rows [first, first+n_new) are written; the candidates' rows (all < first) are read: disjoint
+  return launch_detour_rows(graph, graph + (size_t)first * R, edge_dist + (size_t)first * R, R, P, n_new, cand_ids,
+                            cand_d, nc, st);
 }
 
 static size_t cub_temp_bytes(int64_t m) {

@@ -1,12 +1,14 @@
-// NEXT-1: localized topology-aware repair of severely affected vertices, reading R1
-// in DESIGN.md.  Two kernels over the state at the start of the call (rows of deleted vertices are frozen and only
-// rows of V^L are rewritten, so every row is read unmodified):
+// NEXT-1: localized topology-aware repair of severely affected vertices, reading R1'
+// in DESIGN.md.  Every kernel reads the rows as they were at the start of the call (rows of deleted vertices are
+// frozen, and repaired rows are staged in scratch and scattered only at the end):
 //   repair_mark_kernel   warp per row: deleted fraction of the non-sentinel entries, histogram of Fig. 5 buckets,
 //                        append v to V^L when the fraction exceeds the threshold (strict);
-//   repair_apply_kernel  warp per v in V^L: for each deleted p in row(v) in slot order take the first c members of
+//   repair_union_kernel  warp per v in V^L: for each deleted p in row(v) in slot order take the first c members of
 //                        N_out(p) in slot order that are live, != v, not a live entry of row(v) and not yet taken;
-//                        new row = the R nearest of (live entries with their stored distances, candidates with
-//                        fresh FFMA distances) by (dist, id), sorted (prefix = the P nearest, tail = the rest).
+//                        U = (live entries, stored distances) U (candidates, FFMA distances), its `cap` smallest by
+//                        (dist, id) -> a candidate list exactly like an insertion's;
+//   K-L1 detour select   the insertion's neighbour selection over U into staged rows;
+//   repair_scatter       staged rows -> graph / edge_dist.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -59,13 +61,13 @@ __device__ __forceinline__ void set_put(uint32_t* tab, int bits, uint32_t id) {
   while (atomicCAS(tab + h, kSent, id) != kSent && tab[h] != id) h = (h + 1) & mask;
 }
 
-// ER = registers per lane for a row (R <= 32*ER)
-template <int ER>
+// ER = registers per lane for a row (R <= 32*ER); EU = registers for the union's cap (cap <= 32*EU)
+template <int ER, int EU>
 __global__ void __launch_bounds__(kRepWarps * 32)
-    repair_apply_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist, const float* __restrict__ vec,
-                        int dq, int metric, const uint32_t* __restrict__ tomb, int R, int c,
-                        const uint32_t* __restrict__ list, const unsigned int* __restrict__ n_list, int set_bits,
-                        int cand_cap) {
+    repair_union_kernel(const uint32_t* __restrict__ graph, const float* __restrict__ edge_dist,
+                        const float* __restrict__ vec, int dq, int metric, const uint32_t* __restrict__ tomb, int R,
+                        int c, int cap, const uint32_t* __restrict__ list, int64_t n_list, int set_bits, int cand_cap,
+                        uint32_t* __restrict__ u_ids, float* __restrict__ u_d) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t per_warp = (((size_t)4 << set_bits) + (size_t)cand_cap * 4 + (size_t)cand_cap * 8 + 15) & ~(size_t)15;
@@ -73,19 +75,20 @@ __global__ void __launch_bounds__(kRepWarps * 32)
   uint32_t* tab = reinterpret_cast<uint32_t*>(base);
   uint32_t* cid = tab + (1 << set_bits);
   uint64_t* ckey = reinterpret_cast<uint64_t*>(cid + cand_cap);
-  const unsigned int nv = *n_list;
-  for (unsigned int w = blockIdx.x * kRepWarps + wib; w < nv; w += gridDim.x * kRepWarps) {
+  for (int64_t w = (int64_t)blockIdx.x * kRepWarps + wib; w < n_list; w += (int64_t)gridDim.x * kRepWarps) {
     const uint32_t v = list[w];
     for (int i = lane; i < (1 << set_bits); i += 32) tab[i] = kSent;
     __syncwarp();
     uint32_t rid[ER];
-    uint64_t best[ER];
+    uint64_t best[EU];
+#pragma unroll
+    for (int r = 0; r < EU; ++r) best[r] = kEmptyKey;
 #pragma unroll
     for (int r = 0; r < ER; ++r) {
       const int s = r * 32 + lane;
       rid[r] = s < R ? graph[(size_t)v * R + s] : kSent;
       const bool live = rid[r] != kSent && !tomb_dead(tomb, rid[r]);
-      best[r] = live ? make_key(edge_dist[(size_t)v * R + s], rid[r]) : kEmptyKey;
+      if (r < EU) best[r] = live ? make_key(edge_dist[(size_t)v * R + s], rid[r]) : kEmptyKey;
       if (live) set_put(tab, set_bits, rid[r]);
     }
     __syncwarp();
@@ -138,48 +141,80 @@ __global__ void __launch_bounds__(kRepWarps * 32)
       ckey[i] = make_key((metric == 0 ? acc : -acc) + 0.0f, cid[i]);
     }
     __syncwarp();
-    warp_sort<ER>(best, lane);
+    warp_sort<EU>(best, lane);
     for (int c0 = 0; c0 < ncand; c0 += 32) {
       uint64_t cc[1];
       cc[0] = c0 + lane < ncand ? ckey[c0 + lane] : kEmptyKey;
       warp_sort<1>(cc, lane);
-      warp_merge_into<ER, 1>(best, cc, lane);
+      warp_merge_into<EU, 1>(best, cc, lane);
     }
 #pragma unroll
-    for (int r = 0; r < ER; ++r) {
+    for (int r = 0; r < EU; ++r) {
       const int s = r * 32 + lane;
-      if (s < R) {
-        graph[(size_t)v * R + s] = key_id(best[r]);
-        edge_dist[(size_t)v * R + s] = key_dist(best[r]);
+      if (s < cap) {
+        u_ids[(size_t)w * cap + s] = key_id(best[r]);
+        u_d[(size_t)w * cap + s] = key_dist(best[r]);
       }
     }
     __syncwarp();
   }
 }
 
+__global__ void repair_scatter_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist,
+                                      const uint32_t* __restrict__ list, int64_t n_list, int R,
+                                      const uint32_t* __restrict__ rows, const float* __restrict__ rows_d) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_list * R) return;
+  const int64_t b = t / R;
+  const int s = (int)(t - b * R);
+  graph[(size_t)list[b] * R + s] = rows[t];
+  edge_dist[(size_t)list[b] * R + s] = rows_d[t];
+}
+
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
 }  // namespace
 
-size_t repair_scratch_bytes(int64_t n_alloc) { return (size_t)n_alloc * 4 + 1024; }
+size_t repair_mark_scratch_bytes(int64_t n_alloc) { return al256((size_t)n_alloc * 4) + 256; }
 
-cudaError_t launch_repair(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
-                          const uint32_t* tomb, int R, int64_t n_alloc, int c, double threshold, void* scratch,
-                          size_t scratch_bytes, int num_sms, cudaStream_t st, int64_t* n_repaired,
-                          uint64_t hist_out[5]) {
-  if (n_alloc <= 0) {
-    *n_repaired = 0;
-    for (int i = 0; i < 5; ++i) hist_out[i] = 0;
-    return cudaSuccess;
-  }
-  if (scratch_bytes < repair_scratch_bytes(n_alloc)) return cudaErrorInvalidValue;
+cudaError_t launch_repair_mark(const uint32_t* graph, const uint32_t* tomb, int R, int64_t n_alloc, double threshold,
+                               void* scratch, cudaStream_t st, int64_t* n_list, uint64_t hist_out[5]) {
   uint32_t* list = static_cast<uint32_t*>(scratch);
-  unsigned long long* hist =
-      reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + (((size_t)n_alloc * 4 + 255) & ~(size_t)255));
-  unsigned int* n_list = reinterpret_cast<unsigned int*>(hist + 5);
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) +
+                                                                   al256((size_t)n_alloc * 4));
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(hist + 5);
   cudaError_t e = cudaMemsetAsync(hist, 0, 64, st);
   if (e != cudaSuccess) return e;
-  repair_mark_kernel<<<(unsigned)((n_alloc + 7) / 8), 256, 0, st>>>(graph, tomb, R, n_alloc, threshold, list, n_list,
-                                                                    hist);
+  if (n_alloc > 0)
+    repair_mark_kernel<<<(unsigned)((n_alloc + 7) / 8), 256, 0, st>>>(graph, tomb, R, n_alloc, threshold, list, cnt,
+                                                                      hist);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  unsigned long long hh[6];
+  if ((e = cudaMemcpyAsync(hh, hist, 48, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  for (int i = 0; i < 5; ++i) hist_out[i] = hh[i];
+  *n_list = (int64_t)(hh[5] & 0xFFFFFFFFull);
+  return cudaSuccess;
+}
+
+size_t repair_apply_scratch_bytes(int64_t n_list, int R, int cap) {
+  return 2 * al256((size_t)n_list * cap * 4) + 2 * al256((size_t)n_list * R * 4);
+}
+
+cudaError_t launch_repair_apply(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                                const uint32_t* tomb, int R, int P, int c, int cap, const void* mark_scratch,
+                                int64_t n_list, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t st) {
+  if (n_list <= 0) return cudaSuccess;
+  if (scratch_bytes < repair_apply_scratch_bytes(n_list, R, cap) || cap > 512) return cudaErrorInvalidValue;
+  const uint32_t* list = static_cast<const uint32_t*>(mark_scratch);
+  char* sp = static_cast<char*>(scratch);
+  uint32_t* u_ids = reinterpret_cast<uint32_t*>(sp);
+  sp += al256((size_t)n_list * cap * 4);
+  float* u_d = reinterpret_cast<float*>(sp);
+  sp += al256((size_t)n_list * cap * 4);
+  uint32_t* rows = reinterpret_cast<uint32_t*>(sp);
+  sp += al256((size_t)n_list * R * 4);
+  float* rows_d = reinterpret_cast<float*>(sp);
   const int cand_cap = c * R;
   int set_bits = 1;
   while ((1 << set_bits) < 2 * (R + cand_cap)) ++set_bits;
@@ -188,20 +223,21 @@ cudaError_t launch_repair(uint32_t* graph, float* edge_dist, const float* vec, i
   auto run = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
-    kern<<<(unsigned)(num_sms * 8), kRepWarps * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, c, list,
-                                                                n_list, set_bits, cand_cap);
+    kern<<<(unsigned)(num_sms * 8), kRepWarps * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, c, cap,
+                                                                list, n_list, set_bits, cand_cap, u_ids, u_d);
     return cudaGetLastError();
   };
-  if (R <= 32) e = run(repair_apply_kernel<1>);
-  else if (R <= 64) e = run(repair_apply_kernel<2>);
-  else e = run(repair_apply_kernel<4>);
+  cudaError_t e;
+  const bool big = cap > 128;
+  if (R <= 32) e = big ? run(repair_union_kernel<1, 16>) : run(repair_union_kernel<1, 4>);
+  else if (R <= 64) e = big ? run(repair_union_kernel<2, 16>) : run(repair_union_kernel<2, 4>);
+  else e = big ? run(repair_union_kernel<4, 16>) : run(repair_union_kernel<4, 4>);
   if (e != cudaSuccess) return e;
-  unsigned long long hh[6];
-  if ((e = cudaMemcpyAsync(hh, hist, 48, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-  for (int i = 0; i < 5; ++i) hist_out[i] = hh[i];
-  *n_repaired = (int64_t)(hh[5] & 0xFFFFFFFFull);
-  return cudaSuccess;
+  // the insertion's selection over U, counted on the (unmodified) starting rows, into staged rows
+  if ((e = launch_detour_rows(graph, rows, rows_d, R, P, n_list, u_ids, u_d, cap, st)) != cudaSuccess) return e;
+  repair_scatter_kernel<<<(unsigned)((n_list * R + 255) / 256), 256, 0, st>>>(graph, edge_dist, list, n_list, R, rows,
+                                                                             rows_d);
+  return cudaGetLastError();
 }
 
 }  // namespace svf

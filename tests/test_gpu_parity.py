@@ -296,7 +296,7 @@ def test_repair_bit_exact_integer_data(svf, c1, frac, c, thr):
     X, Q, g, e = c1
     dead = random_tombstones(len(X), frac, seed=int(frac * 100))
     tomb = pack_tomb(dead, len(X))
-    gr, er, nrep, hist = oracle.repair(X, g, e, tomb, c=c, threshold=thr)
+    gr, er, nrep, hist = oracle.repair(X, g, e, tomb, c=c, threshold=thr, cap=128)
     idx = svf.Index.from_state(X, g, e, tomb=tomb)
     out = idx.repair(c=c, threshold=thr)
     st = idx.export()

@@ -413,6 +413,9 @@ def _repair_golden():
 def test_spec_repair_example(orc):
     g, X, G, E = _repair_golden()
     tomb = pack_tomb(g["deleted"], len(X))
+    # (no detours among the union here, so both readings give the distance order)
+    gk, _, _, _ = orc.repair(X, G, E, tomb, c=g["c"], threshold=g["threshold"], mode=0)
+    assert gk[0].tolist() == g["expect_row0"]
     g2, e2, nrep, hist = orc.repair(X, G, E, tomb, c=g["c"], threshold=g["threshold"])
     assert g2[0].tolist() == g["expect_row0"] and e2[0].tolist() == g["expect_d0"]
     assert nrep == 1 and hist.sum() == len(X) - len(g["deleted"])
@@ -424,6 +427,13 @@ def test_spec_repair_example(orc):
     tomb_all = pack_tomb([1, 4, 5, 6], len(X))
     g4, _, _, _ = orc.repair(X, G, E, tomb_all, c=2, threshold=0.3)
     assert g4[0].tolist() == [2, 3, SENT, SENT]
+    # detour selection over the union (R1'): make x list y, so y (count 1) ranks after a and b (count 0)
+    G5 = G.copy()
+    G5[4, 0] = 5
+    g5, e5, _, _ = orc.repair(X, G5, E, tomb, c=g["c"], threshold=g["threshold"])
+    assert g5[0].tolist() == [4, 2, 5, 3] and e5[0].tolist() == [1, 9, 4, 16]   # prefix [x,a] | tail [y,b]
+    gk5, _, _, _ = orc.repair(X, G5, E, tomb, c=g["c"], threshold=g["threshold"], mode=0)
+    assert gk5[0].tolist() == [4, 5, 2, 3]                                         # R1: plain distance order
 
 
 def test_repair_properties_on_a_built_graph(orc):
@@ -441,7 +451,8 @@ def test_repair_properties_on_a_built_graph(orc):
         assert sum(x in deadset for x in old) / len(old) > 0.5       # only severely affected vertices
         new = [int(x) for x in g2[v] if x != SENT]
         assert not (set(new) & deadset) and v not in new and len(set(new)) == len(new)
-        assert list(e2[v][: len(new)]) == sorted(e2[v][: len(new)])
+        tail = [(float(e2[v, s]), int(g2[v, s])) for s in range(R // 2, R) if g2[v, s] != SENT]
+        assert tail == sorted(tail)                                   # prefix detour-ranked, tail sorted
         allowed = set(x for x in old if x not in deadset)
         per_p = {p: [int(x) for x in G[p] if x != SENT] for p in old if p in deadset}
         for x in new:
