@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--dele", type=float, default=0.01, help="fraction of n deleted per round")
     ap.add_argument("--sliding", action="store_true", help="delete the oldest live ids (sliding window)")
     ap.add_argument("--repair", action="store_true")
+    ap.add_argument("--repair-threshold", type=float, default=0.5)
     ap.add_argument("--itopk", type=int, default=32)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -98,14 +99,14 @@ def main():
         rec["delete_ms"] = round(e0.elapsed_time(e1), 3)
         if a.repair:
             t1 = time.perf_counter()
-            out = idx.repair()
+            out = idx.repair(threshold=a.repair_threshold)
             rec["repair_ms"] = round((time.perf_counter() - t1) * 1e3, 3)
             rec["repaired"] = out["repaired"]
             rec["deleted_neighbour_hist"] = out["hist"]
         log.append(rec)
         print(json.dumps(rec), flush=True)
     summ = {"config": a.config, "n": n, "nq": a.nq, "itopk": a.itopk, "rounds": a.rounds, "B_ins": B_ins,
-            "B_del": B_del, "sliding": a.sliding, "repair": a.repair, "gen_s": round(t_gen, 2),
+            "B_del": B_del, "sliding": a.sliding, "repair": a.repair, "repair_threshold": a.repair_threshold, "gen_s": round(t_gen, 2),
             "build_s": round(t_build, 2), "build_inserts_per_s": round(n / t_build),
             "recall_first": log[0]["recall"], "recall_last": log[-1]["recall"],
             "mean_inserts_per_s": round(float(np.mean([x["inserts_per_s"] for x in log if "inserts_per_s" in x]))),
