@@ -90,3 +90,37 @@ def test_c2_insert_and_delete_whole_graph_bit_exact(c2):
     # deleted ids are never returned by a full-batch search afterwards
     ids, _ = idx.search(torch.from_numpy(Q).cuda(), 10, 16)
     assert not np.isin(u32(ids), dead).any()
+
+
+@pytest.fixture(scope="module")
+def c3():
+    """BASELINE configs[2] shape at full size: 10M x 96 unit-norm G-LM (float data), R=64."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2601_08528_b200 as svf
+
+    X = base_rows("C3")
+    Q = query_rows("C3", 2000)
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64)
+    return svf, idx, X, Q
+
+
+def test_c3_float_search_and_knn_sampled(c3):
+    svf, idx, X, Q = c3
+    st = idx.export()
+    sample = np.random.default_rng(3).choice(len(Q), 300, replace=False)
+    gi, gd = idx.knn_exact(torch.from_numpy(Q[sample]).cuda(), 10)
+    gi, gd = u32(gi), gd.cpu().numpy()
+    ri, rd = oracle.bf_knn(X, Q[sample[:12]], 10)                 # exhaustive fp64 scan of 10M rows, 12 queries
+    np.testing.assert_allclose(gd[:12], rd, rtol=1e-4, atol=1e-6)
+    mism = gi[:12] != ri
+    assert np.all(np.abs(gd[:12][mism] - rd[mism]) <= 1e-5 * np.abs(rd[mism]) + 1e-7)
+    for L in (32, 96):
+        ids, d = idx.search(torch.from_numpy(Q[sample]).cuda(), 10, L)
+        ids, d = u32(ids), d.cpu().numpy()
+        oi, od, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, qidx=np.arange(300))
+        r_gpu, r_orc = oracle.recall_ids(ids, gi, 10), oracle.recall_ids(oi, gi, 10)
+        assert abs(r_gpu - r_orc) <= 0.005, (L, r_gpu, r_orc)
+        same = ids == oi
+        assert same.mean() >= 0.99
+        np.testing.assert_allclose(d[same], od[same], rtol=1e-5, atol=1e-7)
