@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* t_full = a_empty + 1;          // [2]
   uint64_t* t_empty = t_full + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  float* wnorm_all = reinterpret_cast<float*>(bars + 64);  // [kTcEpiWarps][32], 16-byte aligned (bars area 512 B)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {  // ---------------- epilogue: thread = query row = TMEM lane, half of the 256 columns ----------------
+    float* wnorm = wnorm_all + (warp - 2) * 32;
     const int lq = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;        // columns [half*128, half*128+128) of every tile
     const int row = lq * 32 + lane;
@@ -240,7 +242,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           __syncwarp();
           tmem_ld32(taddr + c0, v);
           const int64_t cb = nb + half * (TC_N / 2) + c0;
-          const float nrm = (a.metric == 0 && cb + lane < r1) ? __ldg(a.norms + cb + lane) : 0.f;
+          // this chunk's 32 norms, staged per warp for broadcast float4 reads (+inf outside the split)
+          wnorm[lane] = (cb + lane < r1) ? (a.metric == 0 ? __ldg(a.norms + cb + lane) : 0.f)
+                                         : __int_as_float(0x7F800000);
+          __syncwarp();
           // valid columns: inside the split, not deleted, not the query itself
           uint32_t valid = cb >= r1 ? 0u : (r1 - cb >= 32 ? 0xFFFFFFFFu : ((1u << (uint32_t)(r1 - cb)) - 1u));
           if (kTomb && cb < r1) valid &= ~__ldg(a.tomb + (cb >> 5));
@@ -248,17 +253,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int64_t sj = a.self_base + qi - cb;
             if (sj >= 0 && sj < 32) valid &= ~(1u << (uint32_t)sj);
           }
-          // branch-free scores + threshold mask
-          uint32_t pass = 0;
+          // scores and their minimum (2 instructions per column); the pass mask only when some score beats the
+          // current threshold, which is rare once the list has warmed up
+          float mn = __int_as_float(0x7F800000);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float nj = __shfl_sync(0xffffffffu, nrm, j);
-            const float dot = __uint_as_float(v[j]);
-            const float sc = a.metric == 0 ? fmaf(-2.f, dot, nj) : -dot;
-            v[j] = __float_as_uint(sc);
-            pass |= (sc < thr ? 1u : 0u) << j;
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 n4 = reinterpret_cast<const float4*>(wnorm)[j4];
+            const float nj[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int j = j4 * 4 + t;
+              const float dot = __uint_as_float(v[j]);
+              const float sc = a.metric == 0 ? fmaf(-2.f, dot, nj[t]) : (nj[t] == 0.f ? -dot : nj[t]);
+              v[j] = __float_as_uint(sc);
+              mn = fminf(mn, sc);
+            }
           }
-          pass &= valid;
+          uint32_t pass = 0;
+          if (mn < thr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(v[j]) < thr ? 1u : 0u) << j;
+            pass &= valid;
+          }
           while (pass) {  // rare after warm-up: insert into the ascending register list
             const int jj = __ffs(pass) - 1;
             pass &= pass - 1u;
@@ -461,7 +477,7 @@ TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
   TcPlan p;
   p.kc = (dq * 4 + TC_KC - 1) / TC_KC;
   const size_t a_bytes = (size_t)p.kc * kAChunkBytes;
-  const size_t budget = 227 * 1024 - 1024 - 256;
+  const size_t budget = 227 * 1024 - 1024 - 512 - kTcEpiWarps * 32 * 4;
   p.stages = (int)std::min<size_t>(6, (budget - a_bytes) / kBStageBytes);
   p.qtiles = (nq + TC_M - 1) / TC_M;
   const int64_t ntiles = std::max<int64_t>(1, (n + TC_N - 1) / TC_N);
@@ -471,7 +487,7 @@ TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
   p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
   if (p.splits < 1) p.splits = 1;
   p.units = p.qtiles * p.splits;
-  p.smem = 1024 + a_bytes + (size_t)p.stages * kBStageBytes + 256;
+  p.smem = 1024 + a_bytes + (size_t)p.stages * kBStageBytes + 512 + kTcEpiWarps * 32 * 4;
   return p;
 }
 
