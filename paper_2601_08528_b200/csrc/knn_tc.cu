@@ -236,6 +236,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tphase[acc] ^= 1;
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * TC_N + half * (TC_N / 2);
+#ifdef SVF_KNN_NO_EPILOGUE
+        if (true) {
+          tc_fence_before();
+          mbar_arrive(t_empty + acc);
+          acc ^= 1;
+          continue;
+        }
+#endif
 #pragma unroll 1
         for (int c0 = 0; c0 < TC_N / 2; c0 += 32) {
           uint32_t v[32];
