@@ -87,6 +87,29 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// issue a 32-column TMEM load without waiting (pair with tmem_wait32 on the same registers)
+__device__ __forceinline__ void tmem_issue32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+// wait for the outstanding TMEM loads; the registers are in-out operands so no consumer is hoisted above it
+__device__ __forceinline__ void tmem_wait32(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -244,13 +267,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           continue;
         }
 #endif
-#pragma unroll 1
-        for (int c0 = 0; c0 < TC_N / 2; c0 += 32) {
-          uint32_t v[32];
-          __syncwarp();
-          tmem_ld32(taddr + c0, v);
+        // one 32-column chunk: scores, their minimum over 4 independent chains, and (rarely) insertions
+        auto process = [&](uint32_t(&v)[32], int c0) {
           const int64_t cb = nb + half * (TC_N / 2) + c0;
           // this chunk's 32 norms, staged per warp for broadcast float4 reads (+inf outside the split)
+          __syncwarp();
           wnorm[lane] = (cb + lane < r1) ? (a.metric == 0 ? __ldg(a.norms + cb + lane) : 0.f)
                                          : __int_as_float(0x7F800000);
           __syncwarp();
@@ -261,9 +282,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int64_t sj = a.self_base + qi - cb;
             if (sj >= 0 && sj < 32) valid &= ~(1u << (uint32_t)sj);
           }
-          // scores and their minimum (2 instructions per column); the pass mask only when some score beats the
-          // current threshold, which is rare once the list has warmed up
-          float mn = __int_as_float(0x7F800000);
+          float mn4[4] = {__int_as_float(0x7F800000), __int_as_float(0x7F800000), __int_as_float(0x7F800000),
+                          __int_as_float(0x7F800000)};
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
             const float4 n4 = reinterpret_cast<const float4*>(wnorm)[j4];
@@ -274,9 +294,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               const float dot = __uint_as_float(v[j]);
               const float sc = a.metric == 0 ? fmaf(-2.f, dot, nj[t]) : (nj[t] == 0.f ? -dot : nj[t]);
               v[j] = __float_as_uint(sc);
-              mn = fminf(mn, sc);
+              mn4[t] = fminf(mn4[t], sc);
             }
           }
+          const float mn = fminf(fminf(mn4[0], mn4[1]), fminf(mn4[2], mn4[3]));
           uint32_t pass = 0;
           if (mn < thr) {
 #pragma unroll
@@ -305,6 +326,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
           thr = bv[TC_LIST - 1];
+        };
+        // software pipeline over the 4 chunks: the next chunk's TMEM load is in flight while one is processed
+        uint32_t va[32], vb[32];
+        __syncwarp();
+        tmem_issue32(taddr + 0, va);
+        tmem_wait32(va);
+#pragma unroll 1
+        for (int c0 = 0; c0 < TC_N / 2; c0 += 64) {
+          tmem_issue32(taddr + c0 + 32, vb);
+          process(va, c0);
+          tmem_wait32(vb);
+          if (c0 + 64 < TC_N / 2) tmem_issue32(taddr + c0 + 64, va);
+          process(vb, c0 + 32);
+          if (c0 + 64 < TC_N / 2) tmem_wait32(va);
         }
         tc_fence_before();
         mbar_arrive(t_empty + acc);
