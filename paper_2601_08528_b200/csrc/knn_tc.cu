@@ -26,7 +26,7 @@ namespace svf {
 
 namespace {
 
-constexpr int TC_M = 128, TC_N = 256, TC_KC = 32, TC_LIST = 32;
+constexpr int TC_M = 128, TC_N = 256, TC_KC = 32, TC_LIST_MAX = 32;
 constexpr int kTcEpiWarps = 8;                       // 2 per TMEM lane quarter, 128 columns each
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr uint32_t kBStageBytes = TC_N * TC_KC * 4;  // 32 KB
@@ -132,12 +132,14 @@ struct TcArgs {
   const uint32_t* tomb;
   int64_t self_base;     // >= 0: exclude id == self_base + query
   int metric;
-  uint64_t* cand;        // [splits*2][nq][TC_LIST] keys (approx score, id), sorted ascending
+  uint64_t* cand;        // [splits*2][nq][KL] keys (approx score, id), sorted ascending
 };
 
-template <bool kTomb, bool kSelf>
+// KL = per-thread (query row, split, column half) list length: 16 when k <= 16, else 32
+template <bool kTomb, bool kSelf, int KL>
 __global__ void __launch_bounds__(kTcThreads, 1)
     knn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap xmap, TcArgs a) {
+  constexpr int TC_LIST = KL;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned operand area (SWIZZLE_128B atoms)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -384,6 +386,7 @@ __global__ void row_norms_kernel(const float* __restrict__ vec, int dp, int64_t 
 }
 
 // K-R: exact re-rank of the approximate candidates + certificate (warp per query)
+template <int KL>
 __global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t splits, int64_t nq, int k,
                                   const float* __restrict__ vec, int dq, const float* __restrict__ Q,
                                   int64_t q_stride, int q_dim, int metric, const unsigned int* __restrict__ facts,
@@ -397,8 +400,8 @@ __global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t spl
   float tau = __int_as_float(0x7F800000);
   for (int64_t s = 0; s < splits; ++s) {
     uint64_t c[1];
-    c[0] = cand[((size_t)s * nq + qi) * TC_LIST + lane];
-    const uint64_t last = __shfl_sync(0xffffffffu, c[0], 31);
+    c[0] = lane < KL ? cand[((size_t)s * nq + qi) * KL + lane] : kEmptyKey;
+    const uint64_t last = __shfl_sync(0xffffffffu, c[0], KL - 1);
     if (last != kEmptyKey) tau = fminf(tau, key_dist(last));  // a full list excluded rows scoring >= its max
     warp_merge_into<2, 1>(best, c, lane);
   }
@@ -547,7 +550,7 @@ size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
   TcPlan p2 = tc_plan(nq, n, dq, 512);
   const int64_t s = std::max(p.splits, p2.splits);
   // cand + norms + facts + fail list + fallback buffers (rows, ids, dists) + FFMA fallback scratch
-  return (size_t)s * 2 * nq * TC_LIST * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
+  return (size_t)s * 2 * nq * TC_LIST_MAX * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
          (size_t)nq * k * 8 + knn_scratch_bytes(nq, k, n) + 8 * 256;
 }
 
@@ -560,7 +563,8 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   unsigned char* sp = static_cast<unsigned char*>(scratch);
   uint64_t* cand = reinterpret_cast<uint64_t*>(sp);
-  sp += al((size_t)p.splits * 2 * nq * TC_LIST * 8);
+  const int KL = k <= 16 ? 16 : 32;
+  sp += al((size_t)p.splits * 2 * nq * KL * 8);
   float* norms = reinterpret_cast<float*>(sp);
   sp += al((size_t)n * 4);
   unsigned int* facts = reinterpret_cast<unsigned int*>(sp);  // [0] max norm bits, [1] integral, [2] n_fail
@@ -592,13 +596,26 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
     kern<<<grid, kTcThreads, p.smem, st>>>(qmap, xmap, a);
     return cudaGetLastError();
   };
-  if (tomb && self_base >= 0) e = launch(knn_tc_kernel<true, true>);
-  else if (tomb) e = launch(knn_tc_kernel<true, false>);
-  else if (self_base >= 0) e = launch(knn_tc_kernel<false, true>);
-  else e = launch(knn_tc_kernel<false, false>);
+  if (KL == 16) {
+    if (tomb && self_base >= 0) e = launch(knn_tc_kernel<true, true, 16>);
+    else if (tomb) e = launch(knn_tc_kernel<true, false, 16>);
+    else if (self_base >= 0) e = launch(knn_tc_kernel<false, true, 16>);
+    else e = launch(knn_tc_kernel<false, false, 16>);
+  } else {
+    if (tomb && self_base >= 0) e = launch(knn_tc_kernel<true, true, 32>);
+    else if (tomb) e = launch(knn_tc_kernel<true, false, 32>);
+    else if (self_base >= 0) e = launch(knn_tc_kernel<false, true, 32>);
+    else e = launch(knn_tc_kernel<false, false, 32>);
+  }
   if (e != cudaSuccess) return e;
-  knn_rerank_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride, q_dim,
-                                                               metric, facts, out_ids, out_d, fail_list, facts + 2);
+  if (KL == 16)
+    knn_rerank_kernel<16><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride,
+                                                                    q_dim, metric, facts, out_ids, out_d, fail_list,
+                                                                    facts + 2);
+  else
+    knn_rerank_kernel<32><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride,
+                                                                    q_dim, metric, facts, out_ids, out_d, fail_list,
+                                                                    facts + 2);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // exact FFMA fallback for the queries the certificate rejected
   unsigned int hf = 0;
