@@ -197,6 +197,12 @@ struct Smem {
   }
 };
 
+// The table is cleared when an insertion round could push it past this load (numerator over 8); the host keeps
+// H >= 4 * max(pool, round size), so any load <= 3/4 leaves room for a full round.
+#ifndef SVF_HASH_LOAD8
+#define SVF_HASH_LOAD8 4
+#endif
+
 template <int KPL, int CPL, int DQT, int WPQ>
 __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
       const uint32_t step32 = (uint32_t)((pa * 32ull) % n);
       int taken = 0;
       for (uint64_t j0 = 0; j0 < n && taken < a.n_init; j0 += MP) {
-        if (hcount + MP > H / 2) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
+        if (hcount + MP > H * SVF_HASH_LOAD8 / 8) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
         int running = 0, mine = 0;
 #pragma unroll
         for (int r = 0; r < CPL; ++r) {
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
       ++iters;
       n_exp += np;
       const int ncand = np * a.R;
-      if (hcount + ncand > H / 2) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
+      if (hcount + ncand > H * SVF_HASH_LOAD8 / 8) hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
       // S3: this warp's neighbour-row slots (registers r with r % WPQ == h), coalesced; from the speculative
       // registers when the guess was right
       uint32_t rowv[CPL];
