@@ -21,10 +21,11 @@ namespace svf {
 
 namespace {
 
-// insert-if-absent; probes read the slot first and only CAS an empty one (shared atomics are ~2x a load)
+// insert-if-absent (linear probing)
 __device__ __forceinline__ bool hash_insert(uint32_t* tab, int hbits, uint32_t id) {
   const uint32_t mask = (1u << hbits) - 1u;
   uint32_t h = (id * 0x9E3779B1u) >> (32 - hbits);
+#ifdef SVF_HASH_READ_FIRST
   for (;;) {
     const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(tab + h);
     if (cur == id) return false;
@@ -35,6 +36,14 @@ __device__ __forceinline__ bool hash_insert(uint32_t* tab, int hbits, uint32_t i
     }
     h = (h + 1) & mask;
   }
+#else
+  for (;;) {
+    uint32_t prev = atomicCAS(tab + h, kHashEmpty, id);
+    if (prev == kHashEmpty) return true;
+    if (prev == id) return false;
+    h = (h + 1) & mask;
+  }
+#endif
 }
 
 template <int WPQ>
