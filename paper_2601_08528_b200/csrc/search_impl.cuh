@@ -197,18 +197,16 @@ __device__ __forceinline__ void merge_all(const SearchArgs& a, uint64_t (&pool)[
     if (r * 32 + lane >= a.L) pool[r] = kEmptyKey;  // exact pool size L (I6)
 }
 
-template <int CPL, int WPQ>
+// Shared memory: one region per warp, [visited table 2^hbits | parents 8 | query id | survivor ids MP | keys 2xMP |
+// counts].  A query served by W warps uses the first warp's table and query id and every warp's own parents,
+// ids, keys and counts, so one-warp and two-warp (pair) processing share the layout.
+template <int CPL>
 struct Smem {
   static constexpr int MP = 32 * CPL;
-  // per warp: survivor ids [MP], keys [2 parities][MP], counts [2 parities][2]
-  static constexpr size_t warp_bytes = ((size_t)MP * 4 + (size_t)2 * MP * 8 + 16 + 15) & ~(size_t)15;
-  // per query slot: visited table [2^hbits], parents [WPQ][8], query id
-  static size_t __host__ __device__ slot_bytes(int hbits) {
-    return (((size_t)4 << hbits) + (size_t)WPQ * 8 * 4 + 16 + 15) & ~(size_t)15;
-  }
-  static size_t __host__ __device__ block_bytes(int hbits) {
-    return (size_t)(kSearchWarpsPerBlock / WPQ) * slot_bytes(hbits) + kSearchWarpsPerBlock * warp_bytes;
-  }
+  static size_t __host__ __device__ head_bytes(int hbits) { return ((size_t)4 << hbits) + 32 + 16; }
+  static constexpr size_t tail_bytes = (size_t)MP * 4 + (size_t)2 * MP * 8 + 16;
+  static size_t __host__ __device__ warp_bytes(int hbits) { return (head_bytes(hbits) + tail_bytes + 15) & ~(size_t)15; }
+  static size_t __host__ __device__ block_bytes(int hbits) { return kSearchWarpsPerBlock * warp_bytes(hbits); }
 };
 
 // The table is cleared when an insertion round could push it past this load (numerator over 8); the host keeps
@@ -217,36 +215,38 @@ struct Smem {
 #define SVF_HASH_LOAD8 4
 #endif
 
-template <int KPL, int CPL, int DQT, int WPQ>
-__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// Serve queries [base + fetched] while fetched < limit, W warps per query; `g0` = first warp of this group,
+// h = this warp's rank in it, slot = the group's barrier slot.
+template <int KPL, int CPL, int DQT, int W>
+__device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* smem, int g0, int h, int slot,
+                                            unsigned long long* counter, int64_t base, int64_t limit, int lane) {
   constexpr int MP = 32 * CPL;
-  using SM = Smem<CPL, WPQ>;
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int slot = wib / WPQ, h = wib % WPQ;
-  unsigned char* sbase = smem + (size_t)slot * SM::slot_bytes(a.hbits);
-  uint32_t* tab = reinterpret_cast<uint32_t*>(sbase);
-  uint32_t* spar = tab + (1 << a.hbits) + h * 8;  // this warp's copy of the iteration's parents
-  unsigned long long* qslot =
-      reinterpret_cast<unsigned long long*>(sbase + SM::slot_bytes(a.hbits) - 16);
-  unsigned char* wbase[WPQ];
+  using SM = Smem<CPL>;
+  const size_t wb = SM::warp_bytes(a.hbits);
+  unsigned char* lead = smem + (size_t)g0 * wb;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(lead);
+  unsigned long long* qslot = reinterpret_cast<unsigned long long*>(lead + ((size_t)4 << a.hbits) + 32);
+  unsigned char* wbase[W];
 #pragma unroll
-  for (int w = 0; w < WPQ; ++w)
-    wbase[w] = smem + (size_t)(kSearchWarpsPerBlock / WPQ) * SM::slot_bytes(a.hbits) +
-               (size_t)(slot * WPQ + w) * SM::warp_bytes;
-  uint32_t* sid = reinterpret_cast<uint32_t*>(wbase[h]);
+  for (int w = 0; w < W; ++w) wbase[w] = smem + (size_t)(g0 + w) * wb;
+  uint32_t* spar = reinterpret_cast<uint32_t*>(wbase[h] + ((size_t)4 << a.hbits));  // this warp's parents
+  uint32_t* sid = reinterpret_cast<uint32_t*>(wbase[h] + SM::head_bytes(a.hbits));
   const int H = 1 << a.hbits;
   const int T = DQT ? Geo<DQT>::T : a.team;
   const int tl = lane & (T - 1);
-  auto keys_of = [&](int w, int par) { return reinterpret_cast<uint64_t*>(wbase[w] + (size_t)MP * 4) + par * MP; };
-  auto cnts_of = [&](int w) { return reinterpret_cast<int*>(wbase[w] + (size_t)MP * 4 + (size_t)2 * MP * 8); };
-
+  auto keys_of = [&](int w, int par) {
+    return reinterpret_cast<uint64_t*>(wbase[w] + SM::head_bytes(a.hbits) + (size_t)MP * 4) + par * MP;
+  };
+  auto cnts_of = [&](int w) {
+    return reinterpret_cast<int*>(wbase[w] + SM::head_bytes(a.hbits) + (size_t)MP * 4 + (size_t)2 * MP * 8);
+  };
+  constexpr int WPQ = W;
   for (;;) {
-    if (h == 0 && lane == 0) *qslot = atomicAdd(a.work_counter, 1ull);
+    if (h == 0 && lane == 0) *qslot = atomicAdd(counter, 1ull);
     qsync<WPQ>(slot);
-    const unsigned long long qi = *qslot;
-    if (qi >= (unsigned long long)a.nq) break;
+    const unsigned long long qf = *qslot;
+    if (qf >= (unsigned long long)limit) break;
+    const unsigned long long qi = (unsigned long long)base + qf;
 
     // S0: the query fragment this lane needs (zero-padded to Dp), straight from global memory; clear the table
     // the query is staged (coalesced) through the visited table, which is cleared right after (H >= Dp: host)
@@ -435,12 +435,28 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(K
   }
 }
 
+// PHASE_B: after the one-warp queue [0, nq - n_tail) drains, warps pair up (w, w^1) and serve the last n_tail
+// queries in pair mode (shorter per-query latency for the batch tail; identical results).
+template <int KPL, int CPL, int DQT, int WPQ, bool PHASE_B>
+__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t n_main = PHASE_B ? a.nq - a.n_tail : a.nq;
+  run_queries<KPL, CPL, DQT, WPQ>(a, smem, wib - wib % WPQ, wib % WPQ, wib / WPQ, a.work_counter, 0, n_main, lane);
+  if constexpr (PHASE_B) {
+    qsync<2>(wib >> 1);  // both partners have drained the first queue
+    run_queries<KPL, CPL, DQT, 2>(a, smem, wib & ~1, wib & 1, wib >> 1, a.work_counter + 1, n_main, a.n_tail,
+                                  lane);
+  }
+}
+
 }  // namespace
 
-template <int KPL, int CPL, int DQT, int WPQ>
+template <int KPL, int CPL, int DQT, int WPQ, bool PB>
 static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
-  auto kern = search_kernel<KPL, CPL, DQT, WPQ>;
-  const size_t smem = Smem<CPL, WPQ>::block_bytes(a.hbits);
+  auto kern = search_kernel<KPL, CPL, DQT, WPQ, PB>;
+  const size_t smem = Smem<CPL>::block_bytes(a.hbits);
   // per-instantiation cache of the (smem size -> resident blocks) query: keeps the launch path host-light
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0;
@@ -480,9 +496,11 @@ template <int KPL, int CPL, int DQT>
 static cudaError_t launch_wpq(SearchArgs a, int num_sms, cudaStream_t st) {
   // two warps per query only where the candidate slots split evenly (CPL >= 2) and pools are small
   if constexpr (CPL >= 2 && KPL <= 4) {
-    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2>(a, num_sms, st);
+    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2, false>(a, num_sms, st);
+    if (a.n_tail > 0) return launch_kpl_cpl<KPL, CPL, DQT, 1, true>(a, num_sms, st);
   }
-  return launch_kpl_cpl<KPL, CPL, DQT, 1>(a, num_sms, st);
+  a.n_tail = 0;
+  return launch_kpl_cpl<KPL, CPL, DQT, 1, false>(a, num_sms, st);
 }
 
 template <int KPL, int DQT>

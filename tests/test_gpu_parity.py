@@ -306,3 +306,19 @@ def test_repair_bit_exact_integer_data(svf, c1, frac, c, thr):
     ids, d = idx.search(cuda(Q), 10, 32)
     ri, rd, _ = oracle.graph_search(X, gr, Q, 10, 32, tomb=tomb)
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+@pytest.mark.parametrize("wpq", [0, 1, 2])
+def test_search_large_batch_all_modes_bit_exact(svf, c1, wpq):
+    """5000 queries: auto mode (0) runs one warp per query then warp pairs for the batch tail (phase B); 1 and 2 are
+    the pure modes.  All must equal the oracle bit for bit, including the tail queries."""
+    X, Q, g, e = c1
+    from workloads import query_rows as qr
+
+    Qb = qr("C1", 5000)
+    idx = svf.Index.from_state(X, g, e)
+    idx.set_warps_per_query(wpq)
+    ids, d = idx.search(cuda(Qb), 10, 32)
+    ri, rd, rc = oracle.graph_search(X, g, Qb, 10, 32)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+    assert idx.last_search_counters()["iters"] == rc[:, 2].sum()
