@@ -23,7 +23,7 @@ struct svf_index {
   uint32_t* tomb = nullptr;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
-  unsigned long long* small = nullptr;  // [1] newly-deleted, [2] bad flag, [4..5] search queue counters
+  unsigned long long* small = nullptr;  // [1] newly-deleted, [2] bad flag, [4] search queue counter
   uint32_t* counters = nullptr;         // [nq][3] of the last search
   int64_t counters_cap = 0, counters_nq = 0;
   cudaStream_t last_stream = nullptr;
@@ -31,7 +31,6 @@ struct svf_index {
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
   int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
   int wpq = 0;                          // warps per query: 0 auto, 1, 2
-  int tail_per_sm = 12;                 // auto mode: tail queries served by warp pairs, per SM
   uint64_t knn_queries = 0, knn_fallbacks = 0, knn_tc_calls = 0;
   bool prof = false;
   double prof_ms[4] = {0, 0, 0, 0};
@@ -212,13 +211,8 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   // batch fills the resident warps (4096: 0.51 vs 0.57 ms, 10K: 0.85 vs 1.20 ms).  Automatic: 2 while the batch
   // needs at most half of the resident warp slots (~24 per SM), else 1.
   a.wpq = c.wpq;
-  a.n_tail = 0;
-  if (idx->wpq == 0) {
-    a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
-    // large batches: one warp per query, then warp pairs for the batch tail (about one query per resident pair)
-    if (a.wpq == 1) a.n_tail = std::min<int64_t>(nq / 3, (int64_t)idx->tail_per_sm * idx->num_sms);
-  }
-  cudaError_t e = cudaMemsetAsync(idx->small + 4, 0, 2 * sizeof(unsigned long long), st);
+  if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
+  cudaError_t e = cudaMemsetAsync(idx->small + 4, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   cudaEvent_t pa;
   prof_begin(idx, st, &pa);

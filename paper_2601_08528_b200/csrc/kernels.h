@@ -34,8 +34,7 @@ struct SearchArgs {
   uint32_t* out_ids;
   float* out_d;
   uint32_t* counters;      // nullable: [nq][3] = n_dist, iters, n_exp
-  unsigned long long* work_counter;  // [2] queue counters, zeroed before launch
-  int64_t n_tail;          // last n_tail queries served by warp pairs once the one-warp queue drains (0 = off)
+  unsigned long long* work_counter;  // query queue counter, zeroed before launch
   int wpq;                 // warps per query: 1, or 2 (pair mode; used when the candidate slots split evenly)
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);

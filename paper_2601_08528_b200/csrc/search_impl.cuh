@@ -435,27 +435,19 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
   }
 }
 
-// PHASE_B: after the one-warp queue [0, nq - n_tail) drains, warps pair up (w, w^1) and serve the last n_tail
-// queries in pair mode (shorter per-query latency for the batch tail; identical results).
-template <int KPL, int CPL, int DQT, int WPQ, bool PHASE_B>
+template <int KPL, int CPL, int DQT, int WPQ>
 __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t n_main = PHASE_B ? a.nq - a.n_tail : a.nq;
-  run_queries<KPL, CPL, DQT, WPQ>(a, smem, wib - wib % WPQ, wib % WPQ, wib / WPQ, a.work_counter, 0, n_main, lane);
-  if constexpr (PHASE_B) {
-    qsync<2>(wib >> 1);  // both partners have drained the first queue
-    run_queries<KPL, CPL, DQT, 2>(a, smem, wib & ~1, wib & 1, wib >> 1, a.work_counter + 1, n_main, a.n_tail,
-                                  lane);
-  }
+  run_queries<KPL, CPL, DQT, WPQ>(a, smem, wib - wib % WPQ, wib % WPQ, wib / WPQ, a.work_counter, 0, a.nq, lane);
 }
 
 }  // namespace
 
-template <int KPL, int CPL, int DQT, int WPQ, bool PB>
+template <int KPL, int CPL, int DQT, int WPQ>
 static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
-  auto kern = search_kernel<KPL, CPL, DQT, WPQ, PB>;
+  auto kern = search_kernel<KPL, CPL, DQT, WPQ>;
   const size_t smem = Smem<CPL>::block_bytes(a.hbits);
   // per-instantiation cache of the (smem size -> resident blocks) query: keeps the launch path host-light
   static thread_local size_t cached_smem = 0;
@@ -496,11 +488,9 @@ template <int KPL, int CPL, int DQT>
 static cudaError_t launch_wpq(SearchArgs a, int num_sms, cudaStream_t st) {
   // two warps per query only where the candidate slots split evenly (CPL >= 2) and pools are small
   if constexpr (CPL >= 2 && KPL <= 4) {
-    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2, false>(a, num_sms, st);
-    if (a.n_tail > 0) return launch_kpl_cpl<KPL, CPL, DQT, 1, true>(a, num_sms, st);
+    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2>(a, num_sms, st);
   }
-  a.n_tail = 0;
-  return launch_kpl_cpl<KPL, CPL, DQT, 1, false>(a, num_sms, st);
+  return launch_kpl_cpl<KPL, CPL, DQT, 1>(a, num_sms, st);
 }
 
 template <int KPL, int DQT>
