@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no GT / sweep / baselines")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
     ap.add_argument("--wpq", type=int, default=0, help="warps per query (0 = auto)")
+    ap.add_argument("--handoff", type=int, default=-1, help="pair-mode handoff threshold %% (-1 = auto, 0 = off)")
     return ap.parse_args()
 
 
@@ -180,6 +181,7 @@ def run_svf(a):
     del Xd
     idx.set_search_params(a.search_width, 0, 0, a.hash_bits)
     idx.set_warps_per_query(a.wpq)
+    idx.set_search_handoff(a.handoff)
     from paper_2601_08528_b200.sharded import ShardedIndex
 
     sh = ShardedIndex(idx, D.rank, D.world)          # global id g = local * G + r
@@ -371,7 +373,8 @@ def run_svf(a):
                                       (", NCCL all-gather + svf_merge_topk" if D.world > 1 else ""),
                        "value_units": "queries x shards searched per second (== QPS at N=1)"},
             "roofline": roof, "exact_knn": gt_row, "cpu_baseline": cpu, "e2e": e2e, "insert": ins, "clocks": clk,
-            "gpu_launches": a.steps * (1 if D.world == 1 else 2),
+            # search grids per step (one-warp grid [+ chained pair-mode handoff grid]) [+ svf_merge_topk at N>1]
+            "gpu_launches": a.steps * (int(gpu_counters["launches"]) + (0 if D.world == 1 else 1)),
             "setup_s": {"gen": round(t_gen, 2), "build": round(t_build, 2)},
         }
         print(json.dumps(line), flush=True)

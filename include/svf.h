@@ -139,6 +139,14 @@ svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* c
  * are identical for every setting (NEXT-2 low-latency path). */
 svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq);
 
+/* Pair-mode handoff of one-warp batches (NEXT-2 latency path, applied to the batch tail): once the
+ * query queue has drained and fewer than `pct`% of the one-warp grid's warps are still searching, each suspends its
+ * query (pool keys with parent flags + counters) and a second grid, chained by programmatic dependent launch onto
+ * the SM slots the first frees, resumes it with two warps per query.  The visited table restarts from the pool ids,
+ * which leaves the search unchanged (reading I7), so results are identical for every setting.  -1 = automatic,
+ * 0 = off, 1..100.  Applies to pools of <= 128 entries with degree * search_width > 32. */
+svf_status svf_set_search_handoff(svf_index* idx, int32_t pct);
+
 /* Exact-kNN engine: mode 0 = automatic (tcgen05 TF32 scoring + exact FFMA re-rank with a certificate, exact FFMA
  * fallback for rejected queries; used when k <= 32 and query rows are 16-byte aligned), 1 = FFMA tiles only. */
 svf_status svf_set_knn_mode(svf_index* idx, int32_t mode);
@@ -152,8 +160,18 @@ svf_status svf_set_search_params(svf_index* idx, int32_t search_width, int32_t n
                                  int32_t hash_bits);
 
 /* Counters of the last svf_search on this index (synchronises its stream):
- * out[0] = distance computations, out[1] = iterations, out[2] = parents expanded, out[3] = queries. */
-svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]);
+ * out[0] = distance computations, out[1] = iterations, out[2] = parents expanded, out[3] = queries,
+ * out[4] = kernels launched (1, or 2 with the pair-mode handoff grid). */
+svf_status svf_last_search_counters(svf_index* idx, uint64_t out[5]);
+
+/* Per-query timeline of svf_search calls (diagnostics for the batch-tail analysis): after
+ * svf_set_trace(idx, 1), each search records an 8-word row per query i: out[8i] = start and out[8i+1] = end
+ * (device %globaltimer, ns), out[8i+2] = SM id << 32 | iterations, out[8i+3..8i+7] = SM cycles spent in the
+ * select / row-fetch / filter / distance / merge phases (zero unless built with -DSVF_PHASE_PROF).
+ * svf_read_trace copies the last search's rows into the host buffer `out` (cap >= nq rows, else INVALID;
+ * synchronises) and sets *nq (0 if none).  Off by default. */
+svf_status svf_set_trace(svf_index* idx, int32_t enable);
+svf_status svf_read_trace(svf_index* idx, uint64_t* out, int64_t cap, int64_t* nq);
 
 /* Device-time profiling of the main kernel of each call (CUDA events on the caller's stream).
  * svf_profile(idx, 1) enables and resets; svf_profile_read fills ms[0..3] = total ms of

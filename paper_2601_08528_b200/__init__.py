@@ -186,13 +186,31 @@ class Index:
         check(lib().svf_set_search_params(self._h, search_width, n_init, max_iter, hash_bits))
 
     def last_search_counters(self) -> dict:
-        out = (ctypes.c_uint64 * 4)()
+        out = (ctypes.c_uint64 * 5)()
         check(lib().svf_last_search_counters(self._h, out))
-        return {"n_dist": out[0], "iters": out[1], "n_exp": out[2], "queries": out[3]}
+        return {"n_dist": out[0], "iters": out[1], "n_exp": out[2], "queries": out[3], "launches": out[4]}
 
     def set_warps_per_query(self, wpq: int):
         """1 or 2 warps per query (identical results), 0 = automatic."""
         check(lib().svf_set_warps_per_query(self._h, wpq))
+
+    def set_search_handoff(self, pct: int):
+        """Hand a one-warp batch's stragglers to a chained pair-mode grid once fewer than pct% of the warps are
+        still searching (identical results); -1 = automatic, 0 = off."""
+        check(lib().svf_set_search_handoff(self._h, pct))
+
+    def set_trace(self, enable: bool):
+        """Record a per-query timeline (start/end ns, SM, iterations) of later searches (diagnostics)."""
+        check(lib().svf_set_trace(self._h, int(enable)))
+
+    def read_trace(self, max_nq: int):
+        """(start_ns, end_ns, sm, iterations, phase_cycles[n, 5]) of the last traced search (<= max_nq queries)."""
+        buf = np.zeros((max(max_nq, 1), 8), dtype=np.uint64)
+        n = ctypes.c_int64(0)
+        check(lib().svf_read_trace(self._h, buf.ctypes.data, buf.shape[0], ctypes.byref(n)))
+        t = buf[: n.value]
+        return (t[:, 0].astype(np.int64), t[:, 1].astype(np.int64), (t[:, 2] >> np.uint64(32)).astype(np.int64),
+                (t[:, 2] & np.uint64(0xFFFFFFFF)).astype(np.int64), t[:, 3:8].astype(np.int64))
 
     def set_knn_mode(self, mode: int):
         """0 = tcgen05 TF32 scoring + exact re-rank (auto), 1 = FFMA tiles only."""

@@ -5,7 +5,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsvf.so")
+# SVF_LIB selects a tuning variant built by build_lib.build(out=..., extra=...) (experiments only)
+LIB_PATH = os.environ.get("SVF_LIB") or os.path.join(HERE, "libsvf.so")
 
 SVF_OK, SVF_ERR_INVALID, SVF_ERR_CAPACITY, SVF_ERR_NOT_FOUND = 0, 1, 2, 3
 SVF_ERR_CUDA, SVF_ERR_OOM, SVF_ERR_NCCL, SVF_ERR_POISONED = 4, 5, 6, 7
@@ -14,7 +15,7 @@ SENTINEL = 0xFFFFFFFF
 
 EXPORTED = ["svf_default_params", "svf_build", "svf_search", "svf_insert", "svf_delete", "svf_knn_exact",
             "svf_merge_topk", "svf_export", "svf_import", "svf_link_candidates", "svf_set_search_params",
-            "svf_last_search_counters", "svf_set_knn_mode", "svf_knn_stats", "svf_set_warps_per_query", "svf_repair", "svf_profile", "svf_profile_read", "svf_info", "svf_destroy",
+            "svf_last_search_counters", "svf_set_knn_mode", "svf_knn_stats", "svf_set_warps_per_query", "svf_set_search_handoff", "svf_set_trace", "svf_read_trace", "svf_repair", "svf_profile", "svf_profile_read", "svf_info", "svf_destroy",
             "svf_last_error"]
 
 
@@ -62,6 +63,9 @@ def lib() -> ctypes.CDLL:
         "svf_last_search_counters": (ctypes.c_int, [P, ctypes.POINTER(U64)]),
         "svf_set_knn_mode": (ctypes.c_int, [P, I32]),
         "svf_set_warps_per_query": (ctypes.c_int, [P, I32]),
+        "svf_set_search_handoff": (ctypes.c_int, [P, I32]),
+        "svf_set_trace": (ctypes.c_int, [P, I32]),
+        "svf_read_trace": (ctypes.c_int, [P, P, I64, P]),
         "svf_repair": (ctypes.c_int, [P, I32, ctypes.c_double, ctypes.POINTER(I64), ctypes.POINTER(U64), P]),
         "svf_knn_stats": (ctypes.c_int, [P, ctypes.POINTER(U64)]),
         "svf_profile": (ctypes.c_int, [P, I32]),

@@ -16,40 +16,51 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("SVF_NVCC_EXTRA", "").split()
 
 
-def _stale() -> bool:
-    if not os.path.exists(OUT):
+def _stale(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return OUT
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, out: str = OUT, extra: tuple = ()) -> str:
+    """Compile into `out`; `extra` nvcc flags (e.g. -D knobs) build a tuning variant in its own object dir."""
+    if not force and not _stale(out):
+        return out
+    objdir = os.path.join(HERE, "build" + ("" if out == OUT else "_" + os.path.basename(out).replace(".so", "")))
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
+    flagfile = os.path.join(objdir, "flags.txt")
+    flags_same = os.path.exists(flagfile) and open(flagfile).read() == " ".join(FLAGS + list(extra))
+    def hdr_t(src):  # search_impl.cuh is included by the search TUs only
+        return max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS
+                   if src.startswith("search") or h != "search_impl.cuh")
+
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, s), "-o", obj]
+        if (not force and flags_same and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(hdr_t(s), os.path.getmtime(os.path.join(CSRC, s)))):
+            continue                                  # object newer than its source and every header
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = []
     for s, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0 or verbose:
-            sys.stderr.write(out)
+            sys.stderr.write(log)
         if p.returncode != 0:
             failed.append(s)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = OUT + ".tmp"
+    open(flagfile, "w").write(" ".join(FLAGS + list(extra)))
+    tmp = out + ".tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

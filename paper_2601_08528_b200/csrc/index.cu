@@ -2,6 +2,7 @@
 // Every step of the method runs in the kernels of search.cu / link.cu / knn.cu; this file only marshals.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,14 +24,20 @@ struct svf_index {
   uint32_t* tomb = nullptr;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
-  unsigned long long* small = nullptr;  // [1] newly-deleted, [2] bad flag, [4] search queue counter
+  unsigned long long* small = nullptr;  // [1] newly-deleted, [2] bad flag, [4] search queue counter, [5] tail queue
   uint32_t* counters = nullptr;         // [nq][3] of the last search
+  bool trace_on = false;                // per-query timeline of later searches (svf_set_trace)
+  unsigned long long* trace = nullptr;
+  int64_t trace_cap = 0, trace_nq = 0;
   int64_t counters_cap = 0, counters_nq = 0;
   cudaStream_t last_stream = nullptr;
   bool poisoned = false;
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
   int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
   int wpq = 0;                          // warps per query: 0 auto, 1, 2
+  int last_launches = 0;                // kernels launched by the last run_search
+  int ho_pct = -1;                      // pair-mode handoff threshold (% of one-warp warps): -1 auto, 0 off
+  unsigned long long* ho = nullptr;     // handoff control words + slots (handoff_words(), lazily allocated)
   uint64_t knn_queries = 0, knn_fallbacks = 0, knn_tc_calls = 0;
   bool prof = false;
   double prof_ms[4] = {0, 0, 0, 0};
@@ -175,6 +182,17 @@ void prof_resolve(svf_index* idx) {
   idx->prof_pending.clear();
 }
 
+// default handoff threshold: 45% of the one-warp grid's warps (C2, itopk 14, tools/tail_sweep.py: 10K batch
+// 0.836 -> 0.758 ms, 20K 1.359 -> 1.313 ms, 40K 2.553 -> 2.479 ms; 25/35/55% were no better at any batch);
+// SVF_HANDOFF overrides it for tuning
+int handoff_auto() {
+  static const int env = [] {
+    const char* v = getenv("SVF_HANDOFF");
+    return v ? atoi(v) : -1;
+  }();
+  return env >= 0 ? env : 45;
+}
+
 // run K-S on the index: Q (device) with row stride q_stride and q_dim valid floats
 cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_dim, int64_t nq, uint64_t n_snapshot,
                        uint64_t qidx_base, int L, int n_out, const SearchCfg& c, int p, int max_iter,
@@ -205,6 +223,7 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_ids = out_ids;
   a.out_d = out_d;
   a.counters = counters;
+  a.trace = idx->trace_on && counters != nullptr && idx->trace_cap >= nq ? idx->trace : nullptr;
   a.work_counter = idx->small + 4;
   // pair mode (2 warps per query, identical results) cuts per-query latency ~35% (C2 itopk 14: batch 1 p50
   // 0.151 -> 0.091 ms, batch 1024 0.348 -> 0.239 ms; profiles/r01_latency_c2.json) but costs throughput once the
@@ -213,6 +232,22 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.wpq = c.wpq;
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
   cudaError_t e = cudaMemsetAsync(idx->small + 4, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  // one-warp batches: stragglers are handed to a chained pair-mode grid once few warps are left (SearchArgs::ho)
+  a.ho = nullptr;
+  a.ho_thresh = a.wpq == 1 ? (idx->ho_pct >= 0 ? idx->ho_pct : handoff_auto()) : 0;
+  if (a.ho_thresh > 0 && c.kpl <= kHandoffMaxKpl && c.cpl >= 2) {
+    if (idx->ho == nullptr) {
+      e = cudaMalloc(&idx->ho, handoff_words() * 8);
+      if (e != cudaSuccess) return e;
+      e = cudaMemset(idx->ho, 0, handoff_words() * 8);  // slot headers start free; resumed slots are re-freed
+      if (e != cudaSuccess) return e;
+    }
+    a.ho = idx->ho;
+    e = cudaMemsetAsync(idx->ho, 0, 8 * 8, st);       // control words
+    if (e != cudaSuccess) return e;
+  }
+  idx->last_launches = a.ho != nullptr ? 2 : 1;
   if (e != cudaSuccess) return e;
   cudaEvent_t pa;
   prof_begin(idx, st, &pa);
@@ -495,6 +530,14 @@ svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int
     idx->counters_cap = nq;
   }
   idx->counters_nq = nq;
+  if (idx->trace_on && idx->trace_cap < nq) {
+    if (idx->trace) cudaFree(idx->trace);
+    idx->trace = nullptr;
+    idx->trace_cap = 0;
+    CK(idx, cudaMalloc(&idx->trace, (size_t)nq * kTraceCols * 8), "trace");
+    idx->trace_cap = nq;
+  }
+  if (idx->trace_on) idx->trace_nq = nq;
   idx->last_stream = st;
   CK(idx,
      run_search(idx, Qd, idx->D, idx->D, nq, (uint64_t)idx->n_alloc, 0, itopk, k, c, idx->search_width,
@@ -682,13 +725,14 @@ svf_status svf_set_search_params(svf_index* idx, int32_t search_width, int32_t n
   return SVF_OK;
 }
 
-svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
+svf_status svf_last_search_counters(svf_index* idx, uint64_t out[5]) {
   svf_status s = enter(idx);
   if (s != SVF_OK) return s;
   std::lock_guard<std::mutex> lk(idx->mu);
   DeviceGuard g(idx->dev);
   out[0] = out[1] = out[2] = 0;
   out[3] = (uint64_t)idx->counters_nq;
+  out[4] = (uint64_t)idx->last_launches;
   if (idx->counters_nq == 0) return SVF_OK;
   CK(idx, cudaStreamSynchronize(idx->last_stream), "sync");
   std::vector<uint32_t> h((size_t)idx->counters_nq * 3);
@@ -698,6 +742,28 @@ svf_status svf_last_search_counters(svf_index* idx, uint64_t out[4]) {
     out[1] += h[q * 3 + 1];
     out[2] += h[q * 3 + 2];
   }
+  return SVF_OK;
+}
+
+svf_status svf_set_trace(svf_index* idx, int32_t enable) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->trace_on = enable != 0;
+  idx->trace_nq = 0;
+  return SVF_OK;
+}
+
+svf_status svf_read_trace(svf_index* idx, uint64_t* out, int64_t cap, int64_t* nq) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  *nq = idx->trace_nq;
+  if (idx->trace_nq == 0) return SVF_OK;
+  if (cap < idx->trace_nq) return fail(SVF_ERR_INVALID, "trace buffer too small");
+  CK(idx, cudaStreamSynchronize(idx->last_stream), "sync");
+  CK(idx, cudaMemcpy(out, idx->trace, (size_t)idx->trace_nq * kTraceCols * 8, cudaMemcpyDeviceToHost), "D2H trace");
   return SVF_OK;
 }
 
@@ -740,6 +806,15 @@ svf_status svf_set_warps_per_query(svf_index* idx, int32_t wpq) {
   if (wpq < 0 || wpq > 2) return fail(SVF_ERR_INVALID, "warps_per_query must be 0 (auto), 1 or 2");
   std::lock_guard<std::mutex> lk(idx->mu);
   idx->wpq = wpq;
+  return SVF_OK;
+}
+
+svf_status svf_set_search_handoff(svf_index* idx, int32_t pct) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (pct < -1 || pct > 100) return fail(SVF_ERR_INVALID, "handoff threshold must be -1 (auto), 0 (off) or 1..100");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->ho_pct = pct;
   return SVF_OK;
 }
 
@@ -808,6 +883,8 @@ svf_status svf_destroy(svf_index* idx) {
   cudaFree(idx->small);
   cudaFree(idx->scratch);
   cudaFree(idx->counters);
+  if (idx->trace) cudaFree(idx->trace);
+  if (idx->ho) cudaFree(idx->ho);
   if (idx->ev0) cudaEventDestroy(idx->ev0);
   if (idx->ev1) cudaEventDestroy(idx->ev1);
   for (auto& r : idx->prof_pending) {

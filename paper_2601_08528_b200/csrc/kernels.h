@@ -7,11 +7,29 @@
 namespace svf {
 
 constexpr int kSearchWarpsPerBlock = 4;
+constexpr int kTraceCols = 8;  // per-query trace row: start ns, end ns, smid << 32 | iters, 5 phase cycle sums
+constexpr int kHandoffMaxWarps = 148 * 64;  // handoff slots: one per warp of the one-warp grid
+constexpr int kHandoffMaxKpl = 4;           // pools of <= 128 keys (the pair-mode instantiations)
+constexpr size_t handoff_words() { return 8 + (size_t)kHandoffMaxWarps * (4 + 32 * kHandoffMaxKpl); }
 // register cap per pool size: small pools -> more resident warps (latency-bound gathers want occupancy)
 #ifndef SVF_MINB1
 #define SVF_MINB1 6
 #endif
-constexpr int search_min_blocks(int kpl) { return kpl <= 1 ? SVF_MINB1 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2; }
+#ifndef SVF_MINB_PAIR
+#define SVF_MINB_PAIR 4
+#endif
+constexpr int search_min_blocks(int kpl, int wpq = 1) {
+  return wpq == 2 ? SVF_MINB_PAIR : kpl <= 1 ? SVF_MINB1 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2;
+}
+// vectors per distance team per gather round: the throughput (one-warp) kernel keeps 2 (more costs occupancy);
+// the latency kernels (pair mode: small batches and the batch tail) gather deeper per round
+#ifndef SVF_GATHER_U
+#define SVF_GATHER_U 2
+#endif
+#ifndef SVF_GATHER_U_PAIR
+#define SVF_GATHER_U_PAIR 4
+#endif
+constexpr int gather_u(int wpq) { return wpq == 2 ? SVF_GATHER_U_PAIR : SVF_GATHER_U; }
 
 struct SearchArgs {
   const float* vec;        // [cap][dq*4]
@@ -36,6 +54,15 @@ struct SearchArgs {
   uint32_t* counters;      // nullable: [nq][3] = n_dist, iters, n_exp
   unsigned long long* work_counter;  // query queue counter, zeroed before launch
   int wpq;                 // warps per query: 1, or 2 (pair mode; used when the candidate slots split evenly)
+  // Pair-mode handoff (one-warp batches): once the query queue has drained and fewer than ho_thresh of the grid's
+  // ho_total warps are still serving queries, each of them suspends its query (pool keys + counters) into a slot
+  // of `ho`; a pair-mode kernel chained by programmatic dependent launch resumes the suspended queries on the SM
+  // slots the first grid frees, two warps per query, so the batch does not end with long single-warp stragglers.
+  // ho: nullable; [0] slots reserved, [1] unused, [2] slots taken, [3] warps exited, slots from word 8.
+  unsigned long long* ho;
+  int ho_thresh, ho_total;
+  int is_tail;             // set by the launcher on the chained pair-mode (resume) kernel
+  unsigned long long* trace;  // nullable: [nq][kTraceCols] (svf_set_trace, include/svf.h)
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 

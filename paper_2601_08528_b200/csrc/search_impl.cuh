@@ -83,17 +83,29 @@ struct Geo {
 
 // Distances of this warp's S survivors sid[0..S) -> keys; keep those strictly better than the pool's current L-th
 // key (the only ones that can enter: the pool keeps the L smallest of pool U cand), compacted into skey[0..S2).
-template <int KPL, int CPL, int DQT>
+template <int KPL, int CPL, int DQT, int U>
 __device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
                                          uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
-#ifndef SVF_GATHER_U
-#define SVF_GATHER_U 2
-#endif
-  constexpr int U = SVF_GATHER_U;  // vectors per team per round (U * 32/T vectors in flight per warp)
+  // U = vectors per team per round (U * 32/T vectors in flight per warp)
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
   __syncwarp();
+#ifndef SVF_PREFETCH
+#define SVF_PREFETCH 1
+#endif
+#if SVF_PREFETCH == 2
+  // rows beyond the first gather round: one bulk L2 prefetch per row (TMA unit, no registers), so later rounds
+  // hit L2 instead of waiting a full DRAM latency each
+  for (int s = nteams * U + lane; s < S; s += 32)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vec4 + (size_t)sid[s] * DQ), "r"(DQ * 16)
+                 : "memory");
+#elif SVF_PREFETCH == 1
+  for (int i = nteams * U * 4 + lane; i < S * 4; i += 32) {
+    const char* p = reinterpret_cast<const char*>(vec4 + (size_t)sid[i >> 2] * DQ) + (i & 3) * 128;
+    if ((i & 3) * 128 < DQ * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+#endif
   for (int base = 0; base < S; base += nteams * U) {
     float4 xv[U][4];
     uint32_t id[U];
@@ -215,6 +227,26 @@ struct Smem {
 #define SVF_HASH_LOAD8 4
 #endif
 
+// Resume kernel: the next suspended query's slot index, or ~0 once every one-warp warp has left and no reserved
+// slot remains (lane 0 of the query's first warp).
+__device__ __forceinline__ unsigned long long ho_take(const SearchArgs& a, size_t stride) {
+  const unsigned long long i = atomicAdd(a.ho + 2, 1ull);
+  if (i >= (unsigned long long)a.ho_total) return ~0ull;  // at most one suspension per one-warp warp
+  volatile unsigned long long* hs = a.ho + 8 + i * stride;
+  for (;;) {
+    if (hs[0] >> 63) {
+      __threadfence();
+      return i;
+    }
+    if (*reinterpret_cast<volatile unsigned long long*>(a.ho + 3) >= (unsigned long long)a.ho_total) {
+      // every one-warp warp has left (each published its slot before leaving): reservations are final
+      __threadfence();
+      if (i >= *reinterpret_cast<volatile unsigned long long*>(a.ho + 0)) return ~0ull;
+    }
+    __nanosleep(256);
+  }
+}
+
 // Serve queries [base + fetched] while fetched < limit, W warps per query; `g0` = first warp of this group,
 // h = this warp's rank in it, slot = the group's barrier slot.
 template <int KPL, int CPL, int DQT, int W>
@@ -241,12 +273,20 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
     return reinterpret_cast<int*>(wbase[w] + SM::head_bytes(a.hbits) + (size_t)MP * 4 + (size_t)2 * MP * 8);
   };
   constexpr int WPQ = W;
+  const bool resume = WPQ == 2 && a.is_tail;          // chained kernel: continue suspended queries
+  const bool ho_on = WPQ == 1 && a.ho != nullptr;     // one-warp kernel that may suspend its stragglers
+  // one slot layout for every pool size, so headers never alias pool keys left by a launch with another size
+  constexpr size_t ho_stride = 4 + 32 * kHandoffMaxKpl;
+  unsigned long long ho_ex = 0;                       // one-warp warps that have left (lane 0, loaded early)
   for (;;) {
-    if (h == 0 && lane == 0) *qslot = atomicAdd(counter, 1ull);
+    if (h == 0 && lane == 0) *qslot = resume ? ho_take(a, ho_stride) : atomicAdd(counter, 1ull);
     qsync<WPQ>(slot);
     const unsigned long long qf = *qslot;
     if (qf >= (unsigned long long)limit) break;
-    const unsigned long long qi = (unsigned long long)base + qf;
+    unsigned long long* hs = resume ? a.ho + 8 + qf * ho_stride : nullptr;
+    const unsigned long long qi = resume ? (__ldcg(hs) & 0xFFFFFFFFFFull) : (unsigned long long)base + qf;
+    unsigned long long t_start = 0;
+    if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // S0: the query fragment this lane needs (zero-padded to Dp), straight from global memory; clear the table
     // the query is staged (coalesced) through the visited table, which is cleared right after (H >= Dp: host)
@@ -297,7 +337,19 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
 
     // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
     const uint64_t n = a.n_alloc;
-    if (n > 0) {
+    if (resume) {
+      // continue a suspended query: its pool (keys with parent flags) and counters; the visited table restarts
+      // from the pool ids, which leaves the search unchanged (I7: a forgotten non-pool id is rejected again)
+      const unsigned long long c1 = __ldcg(hs + 1);
+      n_dist = (uint32_t)c1;
+      iters = (uint32_t)(c1 >> 32);
+      n_exp = (uint32_t)__ldcg(hs + 2);
+      if (a.trace != nullptr) t_start = __ldcg(hs + 3);
+#pragma unroll
+      for (int r = 0; r < KPL; ++r) pool[r] = __ldcg(hs + 4 + r * 32 + lane);
+      hcount = hash_reset<KPL, WPQ>(tab, a.hbits, pool, lane, h, slot);
+      if (h == 0 && lane == 0) hs[0] = 0;  // both warps have read the slot: free for the next launch
+    } else if (n > 0) {
       uint64_t pa = 0, pb = 0;
       if (lane == 0) perm_params(a.seed, a.qidx_base + qi, n, pa, pb);
       pa = __shfl_sync(0xffffffffu, pa, 0);
@@ -330,13 +382,52 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         }
         const int kept = min(running, a.n_init - taken);
         taken += kept;
-        const int S2 = score_own<KPL, CPL, DQT>(a, pool, sid, keys_of(h, par), mine, qv, lane);
+        const int S2 = score_own<KPL, CPL, DQT, gather_u(WPQ)>(a, pool, sid, keys_of(h, par), mine, qv, lane);
         exchange_merge(mine, S2);
       }
     }
 
     // S2-S7: expand the first p unparented entries until every pool entry is parented (I3, I4)
+#ifdef SVF_PHASE_PROF
+    unsigned long long ph[5] = {0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define SVF_PH(i)                 \
+  {                               \
+    const long long tn = clock64(); \
+    ph[i] += tn - tp;             \
+    tp = tn;                      \
+  }
+#else
+#define SVF_PH(i)
+#endif
+    bool suspended = false;
     for (;;) {
+      if (ho_on) {
+        // the queue has drained and few one-warp warps are left: hand this query to the pair-mode kernel
+        const unsigned long long ex = __shfl_sync(0xffffffffu, ho_ex, 0);
+        if ((unsigned long long)a.ho_total - ex < (unsigned long long)a.ho_thresh) {
+          unsigned long long si = 0;
+          if (lane == 0) si = atomicAdd(a.ho + 0, 1ull);
+          si = __shfl_sync(0xffffffffu, si, 0);
+          unsigned long long* ws = a.ho + 8 + si * ho_stride;
+#pragma unroll
+          for (int r = 0; r < KPL; ++r) ws[4 + r * 32 + lane] = pool[r];
+          if (lane == 0) {
+            ws[1] = (unsigned long long)n_dist | ((unsigned long long)iters << 32);
+            ws[2] = n_exp;
+            ws[3] = t_start;
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            *reinterpret_cast<volatile unsigned long long*>(ws) = qi | (1ull << 63);
+          }
+          suspended = true;
+          break;
+        }
+        if (lane == 0) ho_ex = *reinterpret_cast<volatile unsigned long long*>(a.ho + 3);  // used next iteration
+      }
       if (a.max_iter > 0 && (int)iters == a.max_iter) break;
       int np = 0;
 #pragma unroll
@@ -353,6 +444,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
       }
       if (np == 0) break;
       __syncwarp();
+      SVF_PH(0)
       // The best still-unparented entry is the likely next parent (it stays first unless this iteration's
       // candidates beat it).  p == 1: load its row into registers now, consumed next iteration if the guess holds,
       // so the dependent row fetch overlaps this iteration's vector gathers.  p > 1: pull it toward L2.
@@ -396,6 +488,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
           asm volatile("prefetch.global.L2 [%0];" ::"l"(prow));
         }
       }
+      SVF_PH(1)
       // S4: sentinel / snapshot / tombstone / visited filters on this warp's slots
       int running = 0;
 #pragma unroll
@@ -409,14 +502,17 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         if (ok) sid[running + __popc(m & ((1u << lane) - 1u))] = id;
         running += __popc(m);
       }
+      SVF_PH(2)
       // S5: distances of this warp's survivors; S6: exchange + merge
       if (WPQ == 1 && running == 0) continue;
-      const int S2 = score_own<KPL, CPL, DQT>(a, pool, sid, keys_of(h, par), running, qv, lane);
+      const int S2 = score_own<KPL, CPL, DQT, gather_u(WPQ)>(a, pool, sid, keys_of(h, par), running, qv, lane);
+      SVF_PH(3)
       exchange_merge(running, S2);
+      SVF_PH(4)
     }
 
     // S8: emit the first n_out entries (k, or the whole pool in insert mode)
-    if (h == 0) {
+    if (h == 0 && !suspended) {
 #pragma unroll
       for (int r = 0; r < KPL; ++r) {
         const int e = r * 32 + lane;
@@ -430,66 +526,147 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         a.counters[qi * 3 + 1] = iters;
         a.counters[qi * 3 + 2] = n_exp;
       }
+      if (a.trace != nullptr && lane == 0) {
+        unsigned long long t_end;
+        unsigned int smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* row = a.trace + qi * kTraceCols;
+        row[0] = t_start;
+        row[1] = t_end;
+        row[2] = ((unsigned long long)smid << 32) | iters;
+#ifdef SVF_PHASE_PROF
+        for (int i = 0; i < 5; ++i) row[3 + i] = ph[i];
+#else
+        for (int i = 0; i < 5; ++i) row[3 + i] = 0;
+#endif
+      }
     }
     __syncwarp();
   }
 }
 
 template <int KPL, int CPL, int DQT, int WPQ>
-__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL)) search_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, search_min_blocks(KPL, WPQ)) search_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
+  if (WPQ == 2 && a.is_tail) {
+    // chained resume kernel: continue the suspended queries, then wait for the one-warp grid so that stream order
+    // (the next operation waits for this grid) also covers it
+    run_queries<KPL, CPL, DQT, WPQ>(a, smem, wib - wib % WPQ, wib % WPQ, wib / WPQ, nullptr, 0, INT64_MAX, lane);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  // the chained resume kernel may be launched at once: its blocks take SM slots only as this grid's blocks exit,
+  // i.e. after the queue has drained
+  if (a.ho != nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   run_queries<KPL, CPL, DQT, WPQ>(a, smem, wib - wib % WPQ, wib % WPQ, wib / WPQ, a.work_counter, 0, a.nq, lane);
+  if (WPQ == 1 && a.ho != nullptr && lane == 0) {
+    __threadfence();  // this warp's suspended slot (if any) is published before it counts as gone
+    atomicAdd(a.ho + 3, 1ull);
+  }
 }
 
 }  // namespace
 
+// resident blocks per SM of one instantiation (cached: keeps the launch path host-light) and its shared memory
 template <int KPL, int CPL, int DQT, int WPQ>
-static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
+static cudaError_t blocks_per_sm(const SearchArgs& a, int& per_sm, size_t& smem) {
   auto kern = search_kernel<KPL, CPL, DQT, WPQ>;
-  const size_t smem = Smem<CPL>::block_bytes(a.hbits);
-  // per-instantiation cache of the (smem size -> resident blocks) query: keeps the launch path host-light
+  smem = Smem<CPL>::block_bytes(a.hbits);
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0;
   static thread_local int cached_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  int per_sm = 0;
-  cudaError_t e = cudaSuccess;
   if (cached_smem == smem && cached_dev == dev) {
     per_sm = cached_per_sm;
-  } else {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    // Carveout: the L1 part of the unified array holds the in-flight gather lines, so it must stay large (a max-
-    // shared carveout measured 20% slower); ask for just enough shared memory for the register-limited residency.
-    const int want = search_min_blocks(KPL);
-    const int pct = (int)std::min<size_t>(100, (want * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
-    if (e != cudaSuccess) return e;
-    cached_smem = smem;
-    cached_per_sm = per_sm;
-    cached_dev = dev;
+    return cudaSuccess;
   }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // Carveout: the L1 part of the unified array holds the in-flight gather lines, so it must stay large (a max-
+  // shared carveout measured 20% slower); ask for just enough shared memory for the register-limited residency.
+  const int want = search_min_blocks(KPL, WPQ);
+  const int pct = (int)std::min<size_t>(100, (want * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
+  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  cached_smem = smem;
+  cached_per_sm = per_sm;
+  cached_dev = dev;
+  return cudaSuccess;
+}
+
+template <int KPL, int CPL, int DQT, int WPQ>
+static cudaError_t launch_kpl_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
+  int per_sm = 0;
+  size_t smem = 0;
+  cudaError_t e = blocks_per_sm<KPL, CPL, DQT, WPQ>(a, per_sm, smem);
+  if (e != cudaSuccess) return e;
   long long blocks = (long long)per_sm * num_sms;
   constexpr int qpb = kSearchWarpsPerBlock / WPQ;
   const long long need = (a.nq + qpb - 1) / qpb;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kSearchWarpsPerBlock * 32, smem, st>>>(a);
+  search_kernel<KPL, CPL, DQT, WPQ><<<(unsigned)blocks, kSearchWarpsPerBlock * 32, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+// One-warp grid + chained pair-mode resume grid (handoff of the batch's stragglers, see SearchArgs::ho).
+// a.ho_thresh arrives as a percentage of the one-warp grid's warps.
+template <int KPL, int CPL, int DQT>
+static cudaError_t launch_handoff(SearchArgs a, int num_sms, cudaStream_t st) {
+  int per_sm = 0, per_sm2 = 0;
+  size_t smem = 0, smem2 = 0;
+  cudaError_t e = blocks_per_sm<KPL, CPL, DQT, 1>(a, per_sm, smem);
+  if (e != cudaSuccess) return e;
+  e = blocks_per_sm<KPL, CPL, DQT, 2>(a, per_sm2, smem2);
+  if (e != cudaSuccess) return e;
+  long long blocks = (long long)per_sm * num_sms;
+  const long long need = (a.nq + kSearchWarpsPerBlock - 1) / kSearchWarpsPerBlock;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  a.ho_total = (int)(blocks * kSearchWarpsPerBlock);
+  if (a.ho_total > kHandoffMaxWarps) return launch_kpl_cpl<KPL, CPL, DQT, 1>(a, num_sms, st);  // no slots
+  a.ho_thresh = (int)((long long)a.ho_total * a.ho_thresh / 100);
+  search_kernel<KPL, CPL, DQT, 1><<<(unsigned)blocks, kSearchWarpsPerBlock * 32, smem, st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // programmatic dependent launch: the one-warp grid triggers at its start, so this grid's blocks are pending and
+  // take SM slots as the one-warp grid's blocks exit
+  long long blocks2 = (long long)per_sm2 * num_sms;
+  // at most ho_thresh queries are still in flight when the warps start to suspend: two warps each
+  const long long need2 = ((long long)a.ho_thresh * 2 + kSearchWarpsPerBlock - 1) / kSearchWarpsPerBlock + 1;
+  if (blocks2 > need2) blocks2 = need2;
+  a.is_tail = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)blocks2);
+  cfg.blockDim = dim3(kSearchWarpsPerBlock * 32);
+  cfg.dynamicSmemBytes = smem2;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, search_kernel<KPL, CPL, DQT, 2>, a);
 }
 
 template <int KPL, int CPL, int DQT>
 static cudaError_t launch_wpq(SearchArgs a, int num_sms, cudaStream_t st) {
   // two warps per query only where the candidate slots split evenly (CPL >= 2) and pools are small
   if constexpr (CPL >= 2 && KPL <= 4) {
-    if (a.wpq == 2) return launch_kpl_cpl<KPL, CPL, DQT, 2>(a, num_sms, st);
+    if (a.wpq == 2) {
+      a.ho = nullptr;
+      return launch_kpl_cpl<KPL, CPL, DQT, 2>(a, num_sms, st);
+    }
+    if (a.ho != nullptr && a.ho_thresh > 0) return launch_handoff<KPL, CPL, DQT>(a, num_sms, st);
   }
+  a.ho = nullptr;
   return launch_kpl_cpl<KPL, CPL, DQT, 1>(a, num_sms, st);
 }
 
