@@ -1,0 +1,35 @@
+"""Build + 1%-batch insert rate on C2 (the knob under test comes from the environment, e.g. SVF_HANDOFF, which
+svf_build reads before any per-index setting exists).  Prints one JSON line.
+
+  SVF_HANDOFF=45 python tools/insert_rate.py
+"""
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2601_08528_b200 as svf  # noqa: E402
+from workloads import base_rows  # noqa: E402
+
+X = torch.from_numpy(base_rows("C2")).cuda()
+Xn = torch.from_numpy(base_rows("C2", 1_000_000, 120_000)).cuda()
+torch.cuda.synchronize()
+t0 = time.time()
+idx = svf.Index.build(X, degree=64, capacity=1_120_000)
+torch.cuda.synchronize()
+t_build = time.time() - t0
+idx.insert(Xn[:20_000])
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for i in range(10):
+    idx.insert(Xn[20_000 + i * 10_000: 30_000 + i * 10_000])
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 10
+print(json.dumps({"handoff_env": os.environ.get("SVF_HANDOFF"), "build_s": round(t_build, 3),
+                  "build_inserts_per_s": round(1e6 / t_build), "insert_ms_per_10k": round(ms, 3),
+                  "inserts_per_s": round(1e4 / (ms / 1e3))}))

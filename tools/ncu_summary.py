@@ -82,13 +82,15 @@ def main():
     js = {"note": a.note, "nq": a.nq, "itopk": a.itopk}
     if a.rep:
         js["kernels"] = rep_summary(a.rep)
-        k0 = js["kernels"][0]
-        if isinstance(k0.get("dram__bytes_read.sum"), float):
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            rd = k0["dram__bytes_read.sum"] * scale.get(k0["dram__bytes_read.sum.unit"], 1)
-            wr = k0["dram__bytes_write.sum"] * scale.get(k0["dram__bytes_write.sum.unit"], 1)
-            js["dram_bytes_per_launch"] = rd + wr
-            js["dram_bytes_per_query"] = (rd + wr) / a.nq
+        # one search step = every captured search_kernel grid (the one-warp grid + the chained handoff grid)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        step = [k for k in js["kernels"] if "search_kernel" in k["kernel"]] or js["kernels"][:1]
+        if all(isinstance(k.get("dram__bytes_read.sum"), float) for k in step):
+            tot = sum(k["dram__bytes_read.sum"] * scale.get(k["dram__bytes_read.sum.unit"], 1) +
+                      k["dram__bytes_write.sum"] * scale.get(k["dram__bytes_write.sum.unit"], 1) for k in step)
+            js["dram_bytes_per_launch"] = tot
+            js["dram_bytes_per_query"] = tot / a.nq
+            js["step_kernels"] = len(step)
     if a.launches:
         js["launch_list"] = launch_summary(a.launches)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
