@@ -84,7 +84,15 @@ svf_status svf_build(const svf_params* p, const float* X, int64_t n, void* strea
 /* Search(q, k) (Algorithm 1) for a batch of nq queries (nq x dim, row-major).
  * itopk = L, the internal candidate-pool size (k <= L <= 512; "L >= k").  Writes out_ids[nq][k] and
  * out_dists[nq][k], sorted ascending, padded with (SVF_SENTINEL, +inf) when fewer than k live vectors are
- * reachable.  Deleted vectors are never returned.  Query i seeds its entry points with qidx = i. */
+ * reachable.  Deleted vectors are never returned.  Query i seeds its entry points with qidx = i.
+ * Two-stream overlap ("multiple search streams plus one update stream"): svf_search on
+ * one stream may run on the GPU concurrently with ONE svf_insert / svf_delete / svf_repair on another stream
+ * (the two paths own disjoint scratch, queue counters and handoff buffers).  Visibility rule: each query
+ * snapshots n at its start as the ids whose insertion sub-batch has completed on the device, so it never reaches
+ * or samples a partially linked vertex; a row being rewritten concurrently may be read before or after its
+ * update (every id it holds is < n or filtered); a concurrent delete is seen or not, per word.  Results of a
+ * concurrent search are therefore valid but timing-dependent; with no update in flight they are deterministic.
+ * svf_build, svf_knn_exact, svf_import/export and svf_link_candidates must not overlap other calls. */
 svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int32_t itopk, uint32_t* out_ids,
                       float* out_dists, void* stream);
 

@@ -136,6 +136,16 @@ class Index:
         check(lib().svf_insert(self._h, xp, n, out.ctypes.data, _stream(dev)))
         return out
 
+    def insert_async(self, X):
+        """svf_insert without the id read-back: returns at once after enqueueing on the current stream, so an
+        svf_search issued on another stream overlaps it on the GPU.  The ids are the next n in order
+        (ids are library-assigned and monotone, I14), returned as numpy uint32 without synchronising."""
+        xp, xk, dev = _prep(X, np.float32, torch.float32 if torch else None)
+        n = int(xk.shape[0])
+        first = self.info()["n_alloc"]
+        check(lib().svf_insert(self._h, xp, n, None, _stream(dev)))
+        return np.arange(first, first + n, dtype=np.uint32)
+
     def delete(self, ids) -> int:
         """Delete(x) for a batch of ids (svf_delete).  Returns the number newly deleted."""
         ptr, keep, dev = _prep(ids, np.uint32, torch.int32 if torch else None)

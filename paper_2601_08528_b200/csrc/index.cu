@@ -24,7 +24,11 @@ struct svf_index {
   uint32_t* tomb = nullptr;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
-  unsigned long long* small = nullptr;  // [1] newly-deleted, [2] bad flag, [4] search queue counter, [5] tail queue
+  // [1] newly-deleted, [2] bad flag, [4] svf_search queue counter, [5] update-path (insert) queue counter,
+  // [6] n_visible: ids whose insertion has completed on the device (the concurrent-search snapshot)
+  unsigned long long* small = nullptr;
+  void* sscratch = nullptr;             // svf_search staging (separate from the update path's scratch)
+  size_t sscratch_bytes = 0;
   uint32_t* counters = nullptr;         // [nq][3] of the last search
   bool trace_on = false;                // per-query timeline of later searches (svf_set_trace)
   unsigned long long* trace = nullptr;
@@ -37,7 +41,8 @@ struct svf_index {
   int wpq = 0;                          // warps per query: 0 auto, 1, 2
   int last_launches = 0;                // kernels launched by the last run_search
   int ho_pct = -1;                      // pair-mode handoff threshold (% of one-warp warps): -1 auto, 0 off
-  unsigned long long* ho = nullptr;     // handoff control words + slots (handoff_words(), lazily allocated)
+  unsigned long long* ho = nullptr;     // handoff control words + slots of svf_search (handoff_words(), lazy)
+  unsigned long long* ho_upd = nullptr; // the same for the update path's insert searches
   uint64_t knn_queries = 0, knn_fallbacks = 0, knn_tc_calls = 0;
   bool prof = false;
   double prof_ms[4] = {0, 0, 0, 0};
@@ -99,7 +104,24 @@ bool is_device_ptr(const void* ptr) {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// grow-only scratch; reallocation synchronises the stream first (rare)
+// grow-only scratch; reallocation synchronises the stream first (rare).  The update path (insert, delete, repair,
+// build, exact kNN) uses `scratch`; svf_search stages through its own `sscratch`, so a search on one stream never
+// shares a buffer with an update on another.
+cudaError_t grow(void*& buf, size_t& have, size_t bytes, cudaStream_t st) {
+  if (bytes <= have) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  if (buf) cudaFree(buf);
+  buf = nullptr;
+  have = 0;
+  e = cudaMalloc(&buf, bytes);
+  if (e != cudaSuccess) return e;
+  have = bytes;
+  return cudaSuccess;
+}
+cudaError_t ensure_sscratch(svf_index* idx, size_t bytes, cudaStream_t st) {
+  return grow(idx->sscratch, idx->sscratch_bytes, std::max(bytes, (size_t)8 << 20), st);
+}
 cudaError_t ensure_scratch(svf_index* idx, size_t bytes, cudaStream_t st) {
   if (bytes <= idx->scratch_bytes) return cudaSuccess;
   cudaError_t e = cudaStreamSynchronize(st);
@@ -196,7 +218,8 @@ int handoff_auto() {
 // run K-S on the index: Q (device) with row stride q_stride and q_dim valid floats
 cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_dim, int64_t nq, uint64_t n_snapshot,
                        uint64_t qidx_base, int L, int n_out, const SearchCfg& c, int p, int max_iter,
-                       uint32_t* out_ids, float* out_d, uint32_t* counters, int prof_slot, cudaStream_t st) {
+                       uint32_t* out_ids, float* out_d, uint32_t* counters, int prof_slot, cudaStream_t st,
+                       bool update_path) {
   SearchArgs a{};
   a.vec = idx->vec;
   a.dq = idx->dq;
@@ -224,27 +247,31 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_d = out_d;
   a.counters = counters;
   a.trace = idx->trace_on && counters != nullptr && idx->trace_cap >= nq ? idx->trace : nullptr;
-  a.work_counter = idx->small + 4;
+  // the two paths own disjoint queue counters and handoff buffers, so an svf_search on one stream may overlap an
+  // update on another; svf_search snapshots n at each query's start from n_visible
+  a.work_counter = idx->small + (update_path ? 5 : 4);
+  a.n_visible = update_path ? nullptr : idx->small + 6;
   // pair mode (2 warps per query, identical results) cuts per-query latency ~35% (C2 itopk 14: batch 1 p50
   // 0.151 -> 0.091 ms, batch 1024 0.348 -> 0.239 ms; profiles/r01_latency_c2.json) but costs throughput once the
   // batch fills the resident warps (4096: 0.51 vs 0.57 ms, 10K: 0.85 vs 1.20 ms).  Automatic: 2 while the batch
   // needs at most half of the resident warp slots (~24 per SM), else 1.
   a.wpq = c.wpq;
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
-  cudaError_t e = cudaMemsetAsync(idx->small + 4, 0, sizeof(unsigned long long), st);
+  cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
+  unsigned long long*& hob = update_path ? idx->ho_upd : idx->ho;
   // one-warp batches: stragglers are handed to a chained pair-mode grid once few warps are left (SearchArgs::ho)
   a.ho = nullptr;
   a.ho_thresh = a.wpq == 1 ? (idx->ho_pct >= 0 ? idx->ho_pct : handoff_auto()) : 0;
   if (a.ho_thresh > 0 && c.kpl <= kHandoffMaxKpl && c.cpl >= 2) {
-    if (idx->ho == nullptr) {
-      e = cudaMalloc(&idx->ho, handoff_words() * 8);
+    if (hob == nullptr) {
+      e = cudaMalloc(&hob, handoff_words() * 8);
       if (e != cudaSuccess) return e;
-      e = cudaMemset(idx->ho, 0, handoff_words() * 8);  // slot headers start free; resumed slots are re-freed
+      e = cudaMemset(hob, 0, handoff_words() * 8);  // slot headers start free; resumed slots are re-freed
       if (e != cudaSuccess) return e;
     }
-    a.ho = idx->ho;
-    e = cudaMemsetAsync(idx->ho, 0, 8 * 8, st);       // control words
+    a.ho = hob;
+    e = cudaMemsetAsync(hob, 0, 8 * 8, st);       // control words
     if (e != cudaSuccess) return e;
   }
   idx->last_launches = a.ho != nullptr ? 2 : 1;
@@ -324,7 +351,7 @@ svf_status alloc_index(const svf_params* p, svf_index** out) {
       (e = cudaMalloc(&idx->graph, cap * idx->R * 4)) != cudaSuccess ||
       (e = cudaMalloc(&idx->edge_dist, cap * idx->R * 4)) != cudaSuccess ||
       (e = cudaMalloc(&idx->tomb, (cap + 31) / 32 * 4)) != cudaSuccess ||
-      (e = cudaMalloc(&idx->small, 64)) != cudaSuccess ||
+      (e = cudaMalloc(&idx->small, 64)) != cudaSuccess || (e = cudaMemset(idx->small, 0, 64)) != cudaSuccess ||
       (e = cudaMemset(idx->tomb, 0, (cap + 31) / 32 * 4)) != cudaSuccess ||
       (e = cudaEventCreate(&idx->ev0)) != cudaSuccess || (e = cudaEventCreate(&idx->ev1)) != cudaSuccess) {
     svf_destroy(idx);
@@ -356,7 +383,7 @@ svf_status insert_present_rows(svf_index* idx, int64_t n, cudaStream_t st) {
     // (i) insert-mode search over the snapshot: the sub-batch's own rows are neither reachable nor sampled
     CK(idx,
        run_search(idx, idx->vec + (size_t)snap * idx->Dp, idx->Dp, idx->Dp, bsz, (uint64_t)snap, (uint64_t)snap, L,
-                  L, c, idx->p.search_width, idx->p.max_iter, cid, cd, nullptr, 1, st),
+                  L, c, idx->p.search_width, idx->p.max_iter, cid, cd, nullptr, 1, st, true),
        "insert search");
     // (ii) detour-ranked forward rows
     CK(idx, timed(idx, 2, st, [&] {
@@ -368,6 +395,8 @@ svf_status insert_present_rows(svf_index* idx, int64_t n, cudaStream_t st) {
                                snap, bsz, rev, idx->scratch_bytes - 2 * cand_bytes, st);
        }), "reverse edges");
     done += bsz;
+    // the sub-batch is linked: concurrent searches may now see it
+    CK(idx, launch_store_u64(idx->small + 6, (uint64_t)(snap + bsz), st), "publish n_visible");
   }
   idx->n_alloc += n;
   return SVF_OK;
@@ -447,7 +476,9 @@ svf_status svf_build(const svf_params* p, const float* X, int64_t n, void* strea
     s = insert_present_rows(idx, n - n0, st);
     if (s != SVF_OK) return bail(s);
   }
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(nullptr, e, "build"));
+  if ((e = launch_store_u64(idx->small + 6, (uint64_t)idx->n_alloc, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return bail(cuda_fail(nullptr, e, "build"));
   *out = idx;
   return SVF_OK;
 }
@@ -485,6 +516,7 @@ svf_status svf_import(const svf_params* p, const float* vec, const uint32_t* gra
       e = cudaMemcpy(idx->tomb, h.data(), words * 4, cudaMemcpyHostToDevice);
     }
   }
+  if (e == cudaSuccess) e = launch_store_u64(idx->small + 6, (uint64_t)n_alloc, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     svf_destroy(idx);
@@ -513,8 +545,8 @@ svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int
   const bool q_dev = is_device_ptr(Q), i_dev = is_device_ptr(out_ids), d_dev = is_device_ptr(out_dists);
   const size_t qb = q_dev ? 0 : al((size_t)nq * idx->D * 4);
   const size_t ob = al((size_t)nq * k * 4);
-  CK(idx, ensure_scratch(idx, qb + 2 * ob, st), "search scratch");
-  char* sp = static_cast<char*>(idx->scratch);
+  CK(idx, ensure_sscratch(idx, qb + 2 * ob, st), "search scratch");
+  char* sp = static_cast<char*>(idx->sscratch);
   const float* Qd = Q;
   if (!q_dev) {
     CK(idx, cudaMemcpyAsync(sp, Q, (size_t)nq * idx->D * 4, cudaMemcpyHostToDevice, st), "H2D queries");
@@ -541,7 +573,7 @@ svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int
   idx->last_stream = st;
   CK(idx,
      run_search(idx, Qd, idx->D, idx->D, nq, (uint64_t)idx->n_alloc, 0, itopk, k, c, idx->search_width,
-                idx->max_iter, oi, od, idx->counters, 0, st),
+                idx->max_iter, oi, od, idx->counters, 0, st, false),
      "search kernel");
   if (!i_dev) CK(idx, cudaMemcpyAsync(out_ids, oi, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
   if (!d_dev) CK(idx, cudaMemcpyAsync(out_dists, od, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
@@ -882,9 +914,11 @@ svf_status svf_destroy(svf_index* idx) {
   cudaFree(idx->tomb);
   cudaFree(idx->small);
   cudaFree(idx->scratch);
+  if (idx->sscratch) cudaFree(idx->sscratch);
   cudaFree(idx->counters);
   if (idx->trace) cudaFree(idx->trace);
   if (idx->ho) cudaFree(idx->ho);
+  if (idx->ho_upd) cudaFree(idx->ho_upd);
   if (idx->ev0) cudaEventDestroy(idx->ev0);
   if (idx->ev1) cudaEventDestroy(idx->ev1);
   for (auto& r : idx->prof_pending) {

@@ -63,6 +63,9 @@ struct SearchArgs {
   int ho_thresh, ho_total;
   int is_tail;             // set by the launcher on the chained pair-mode (resume) kernel
   unsigned long long* trace;  // nullable: [nq][kTraceCols] (svf_set_trace, include/svf.h)
+  // nullable: device word holding the ids whose insertion has completed; each query snapshots
+  // n = min(n_alloc, *n_visible) at its start (svf_search overlapping an insert on another stream)
+  const unsigned long long* n_visible;
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 
@@ -77,6 +80,9 @@ cudaError_t launch_detour_rows(const uint32_t* graph, uint32_t* out_ids, float* 
 size_t reverse_scratch_bytes(int64_t n_new, int R);
 cudaError_t launch_reverse(uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R, int P, int64_t first,
                            int64_t n_new, void* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// *p = v in stream order (publishes n_visible after an insert sub-batch is linked)
+cudaError_t launch_store_u64(unsigned long long* p, uint64_t v, cudaStream_t st);
 
 // K-D: tombstones.  check pass: *bad = 1 if any id >= n_alloc.  set pass: *newly += newly set bits.
 cudaError_t launch_tomb_check(const uint32_t* ids, int64_t n, uint64_t n_alloc, unsigned int* bad, cudaStream_t st);

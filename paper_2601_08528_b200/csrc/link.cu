@@ -401,4 +401,14 @@ cudaError_t launch_fill_rows(uint32_t* graph, float* edge_dist, int64_t first, i
   return cudaGetLastError();
 }
 
+__global__ void store_u64_kernel(unsigned long long* p, unsigned long long v) {
+  __threadfence();  // the stream's earlier writes (rows, edges) are visible before the published count
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+cudaError_t launch_store_u64(unsigned long long* p, uint64_t v, cudaStream_t st) {
+  store_u64_kernel<<<1, 1, 0, st>>>(p, (unsigned long long)v);
+  return cudaGetLastError();
+}
+
 }  // namespace svf

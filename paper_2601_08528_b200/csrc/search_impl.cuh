@@ -279,9 +279,22 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
   constexpr size_t ho_stride = 4 + 32 * kHandoffMaxKpl;
   unsigned long long ho_ex = 0;                       // one-warp warps that have left (lane 0, loaded early)
   for (;;) {
-    if (h == 0 && lane == 0) *qslot = resume ? ho_take(a, ho_stride) : atomicAdd(counter, 1ull);
+    if (h == 0 && lane == 0) {
+      const unsigned long long f = resume ? ho_take(a, ho_stride) : atomicAdd(counter, 1ull);
+      qslot[0] = f;
+      // the query's snapshot: ids below n exist (n_visible: inserts completed on another stream); resumed queries
+      // keep the snapshot they started with
+      unsigned long long nq = a.n_alloc;
+      if (resume) {
+        if (f != ~0ull) nq = __ldcg(a.ho + 8 + f * ho_stride + 2) >> 32;
+      } else if (a.n_visible != nullptr) {
+        nq = min(nq, *reinterpret_cast<const volatile unsigned long long*>(a.n_visible));
+      }
+      qslot[1] = nq;
+    }
     qsync<WPQ>(slot);
-    const unsigned long long qf = *qslot;
+    const unsigned long long qf = qslot[0];
+    const uint32_t n = (uint32_t)qslot[1];  // ids are u32 below the sentinel: n < 2^32
     if (qf >= (unsigned long long)limit) break;
     unsigned long long* hs = resume ? a.ho + 8 + qf * ho_stride : nullptr;
     const unsigned long long qi = resume ? (__ldcg(hs) & 0xFFFFFFFFFFull) : (unsigned long long)base + qf;
@@ -336,14 +349,13 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
     };
 
     // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
-    const uint64_t n = a.n_alloc;
     if (resume) {
       // continue a suspended query: its pool (keys with parent flags) and counters; the visited table restarts
       // from the pool ids, which leaves the search unchanged (I7: a forgotten non-pool id is rejected again)
       const unsigned long long c1 = __ldcg(hs + 1);
       n_dist = (uint32_t)c1;
       iters = (uint32_t)(c1 >> 32);
-      n_exp = (uint32_t)__ldcg(hs + 2);
+      n_exp = (uint32_t)__ldcg(hs + 2);  // (high half: the snapshot n, read at the fetch)
       if (a.trace != nullptr) t_start = __ldcg(hs + 3);
 #pragma unroll
       for (int r = 0; r < KPL; ++r) pool[r] = __ldcg(hs + 4 + r * 32 + lane);
@@ -414,7 +426,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
           for (int r = 0; r < KPL; ++r) ws[4 + r * 32 + lane] = pool[r];
           if (lane == 0) {
             ws[1] = (unsigned long long)n_dist | ((unsigned long long)iters << 32);
-            ws[2] = n_exp;
+            ws[2] = (unsigned long long)n_exp | ((unsigned long long)n << 32);
             ws[3] = t_start;
           }
           __threadfence();

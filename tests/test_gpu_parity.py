@@ -363,3 +363,41 @@ def test_search_handoff_mixed_pool_sizes(svf, c1):
         ids, d = idx.search(cuda(Qb), 10, L)
         ri, rd, _ = oracle.graph_search(X, g, Qb, 10, L)
         assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd), L
+
+
+def test_search_overlapping_insert_on_two_streams(svf, c1):
+    """NEXT-2 two-stream overlap: an svf_search on stream S issued while an svf_insert runs on
+    stream U.  Visibility rule: each query sees the ids whose insertion had completed on the device when it
+    started (n_visible), never a partially linked sub-batch.  Checked: the concurrent search returns valid results
+    (distinct live ids below the final n_alloc, exact distances, sorted); the insert's graph is bit-identical to a
+    serial insert (searches only read); after both finish, search equals the oracle on the final state again."""
+    X, Q, g, e = c1
+    from workloads import base_rows as br, query_rows as qr
+
+    Xn = br("C1", 10_000, 6_000)
+    Qb = qr("C1", 4000)
+    cap = len(X) + len(Xn)
+    serial = svf.Index.from_state(X, g, e, capacity=cap)
+    serial.insert(cuda(Xn))
+    ref = serial.export()
+    idx = svf.Index.from_state(X, g, e, capacity=cap)
+    s_u, s_q = torch.cuda.Stream(), torch.cuda.Stream()
+    Xd, Qd = cuda(Xn), cuda(Qb)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s_u):
+        new_ids = idx.insert_async(Xd)
+    with torch.cuda.stream(s_q):
+        ids, d = idx.search(Qd, 10, 32)
+    torch.cuda.synchronize()
+    assert np.array_equal(new_ids, np.arange(10_000, 16_000, dtype=np.uint32))
+    st = idx.export()
+    assert np.array_equal(st["graph"], ref["graph"]) and np.array_equal(st["edge_dist"], ref["edge_dist"])
+    ids, d = u32(ids), f32(d)
+    allX = np.concatenate([X, Xn]).astype(np.float64)
+    assert (ids < cap).all() and (np.diff(d, axis=1) >= 0).all()
+    assert all(len(set(r)) == len(r) for r in ids)
+    exact = ((allX[ids] - Qb.astype(np.float64)[:, None, :]) ** 2).sum(-1).astype(np.float32)
+    assert np.array_equal(exact, d)
+    ri, rd, _ = oracle.graph_search(st["vec"], st["graph"], Qb, 10, 32)
+    ids2, d2 = idx.search(Qd, 10, 32)
+    assert np.array_equal(u32(ids2), ri) and np.array_equal(f32(d2), rd)
