@@ -112,7 +112,7 @@ svf_status svf_delete(svf_index* idx, const uint32_t* ids, int64_t n, int64_t* n
 svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, uint32_t* out_ids,
                          float* out_dists, void* stream);
 
-/* Localized topology-aware repair (reading R1' in DESIGN.md): every live vertex whose
+/* Localized topology-aware repair (reading R1' in DESIGN.md; 1 <= c <= degree): every live vertex whose
  * non-empty neighbour slots are more than `threshold` (paper: 0.5) deleted gets, for each deleted neighbour p (slot
  * order), the first c (paper: 8) live members of N_out(p) that are not itself and not already its neighbours;
  * its row is rebuilt by the insertion's selection rule (detour counts, protected prefix + sorted tail) over the
@@ -120,6 +120,21 @@ svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, 
  * {0, (0,0.1), [0.1,0.4], (0.4,threshold], >threshold} (the distribution of Fig. 5).  Synchronous. */
 svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
                       void* stream);
+
+/* Global consolidation (reading C1 in DESIGN.md): "a global consolidation of all
+ * affected neighborhoods by aggregating candidates from the outgoing neighbors of deleted vertices" — every live
+ * vertex with at least one deleted neighbour is rebuilt as by svf_repair with c = degree (all live members of each
+ * deleted neighbour's list) and threshold 0.  Afterwards no live row references a deleted vertex.  *n_rewritten
+ * (nullable) = rows rewritten.  Synchronous; may overlap an svf_search on another stream (see svf_search). */
+svf_status svf_consolidate(svf_index* idx, int64_t* n_rewritten, void* stream);
+
+/* Automatic consolidation: after an svf_delete, when the vertices deleted since the last consolidation exceed
+ * `ratio` times the vertices that were live then ("e.g., 20%"), the delete call consolidates on its
+ * stream.  0 = off (default), else in (0, 1). */
+svf_status svf_set_consolidation(svf_index* idx, double ratio);
+
+/* out[0] = consolidations run so far (explicit + automatic), out[1] = n_deleted at the last one. */
+svf_status svf_consolidation_stats(svf_index* idx, int64_t out[2]);
 
 /* Merge G per-shard top-k lists (ids/dists laid out [G][nq][k], GLOBAL ids) into the first k by (dist, id)
  * per query (the step after the NCCL all-gather).  Uses the current device. */

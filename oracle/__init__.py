@@ -183,6 +183,16 @@ def repair(X, graph, edge_dist, tomb, c: int = 8, threshold: float = 0.5, metric
     return graph, edge_dist, nrep.value, hist
 
 
+def consolidate(X, graph, edge_dist, tomb, metric: int = 0, n_alloc: Optional[int] = None, P: Optional[int] = None,
+                cap: int = 128):
+    """NEXT-4 global consolidation ("aggregating candidates from the outgoing neighbors of deleted
+    vertices"; reading C1): orc_repair with c = R (every live member of each deleted neighbour's list) and
+    threshold 0 (every live vertex with a deleted neighbour).  Returns (graph, edge_dist, n_rewritten)."""
+    R = np.asarray(graph).shape[1]
+    g, e, n, _ = repair(X, graph, edge_dist, tomb, c=R, threshold=0.0, metric=metric, n_alloc=n_alloc, P=P, cap=cap)
+    return g, e, n
+
+
 def merge_topk(ids, d):
     """O6: ids/d of shape [G][nq][k] (global ids) -> first k by key per query."""
     ids, d = _u32(ids), _f32(d)

@@ -53,6 +53,13 @@ def _stream(device) -> Optional[int]:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _cur_stream() -> Optional[int]:
+    """The current CUDA stream (for calls without a tensor argument), or the default stream without torch."""
+    if torch is None or not torch.cuda.is_available():
+        return None
+    return torch.cuda.current_stream().cuda_stream
+
+
 def _empty(shape, np_dtype, torch_dtype, device):
     if device == "pinned":  # pinned host in -> pinned host out (the end-to-end path)
         t = torch.empty(shape, dtype=torch_dtype, pin_memory=True)
@@ -158,8 +165,25 @@ class Index:
         """Localized topology-aware repair of severely affected vertices (svf_repair)."""
         n = ctypes.c_int64()
         hist = (ctypes.c_uint64 * 5)()
-        check(lib().svf_repair(self._h, c, threshold, ctypes.byref(n), hist, None))
+        check(lib().svf_repair(self._h, c, threshold, ctypes.byref(n), hist, _cur_stream()))
         return {"repaired": n.value, "hist": list(hist)}
+
+    def consolidate(self) -> int:
+        """Global consolidation (svf_consolidate): every live row with a deleted neighbour is rebuilt
+        from all live members of its deleted neighbours' lists.  Returns the rows rewritten."""
+        n = ctypes.c_int64()
+        check(lib().svf_consolidate(self._h, ctypes.byref(n), _cur_stream()))
+        return n.value
+
+    def set_consolidation(self, ratio: float):
+        """Consolidate automatically after a delete once the deletions since the last consolidation exceed
+        `ratio` of the vertices live then ("e.g., 20%"); 0 = off."""
+        check(lib().svf_set_consolidation(self._h, float(ratio)))
+
+    def consolidation_stats(self) -> dict:
+        out = (ctypes.c_int64 * 2)()
+        check(lib().svf_consolidation_stats(self._h, out))
+        return {"consolidations": out[0], "deleted_at_last": out[1]}
 
     def knn_exact(self, Q, k: int):
         """Exact k-NN over the live set (svf_knn_exact; ground truth)."""

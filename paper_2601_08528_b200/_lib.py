@@ -15,7 +15,7 @@ SENTINEL = 0xFFFFFFFF
 
 EXPORTED = ["svf_default_params", "svf_build", "svf_search", "svf_insert", "svf_delete", "svf_knn_exact",
             "svf_merge_topk", "svf_export", "svf_import", "svf_link_candidates", "svf_set_search_params",
-            "svf_last_search_counters", "svf_set_knn_mode", "svf_knn_stats", "svf_set_warps_per_query", "svf_set_search_handoff", "svf_set_trace", "svf_read_trace", "svf_repair", "svf_profile", "svf_profile_read", "svf_info", "svf_destroy",
+            "svf_last_search_counters", "svf_set_knn_mode", "svf_knn_stats", "svf_set_warps_per_query", "svf_set_search_handoff", "svf_set_trace", "svf_read_trace", "svf_repair", "svf_consolidate", "svf_set_consolidation", "svf_consolidation_stats", "svf_profile", "svf_profile_read", "svf_info", "svf_destroy",
             "svf_last_error"]
 
 
@@ -68,6 +68,9 @@ def lib() -> ctypes.CDLL:
         "svf_read_trace": (ctypes.c_int, [P, P, I64, P]),
         "svf_repair": (ctypes.c_int, [P, I32, ctypes.c_double, ctypes.POINTER(I64), ctypes.POINTER(U64), P]),
         "svf_knn_stats": (ctypes.c_int, [P, ctypes.POINTER(U64)]),
+        "svf_consolidate": (ctypes.c_int, [P, ctypes.POINTER(I64), P]),
+        "svf_set_consolidation": (ctypes.c_int, [P, ctypes.c_double]),
+        "svf_consolidation_stats": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
         "svf_profile": (ctypes.c_int, [P, I32]),
         "svf_profile_read": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
         "svf_info": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),

@@ -39,6 +39,9 @@ struct svf_index {
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
   int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
   int wpq = 0;                          // warps per query: 0 auto, 1, 2
+  double consolidate_ratio = 0.0;       // NEXT-4 trigger: deletions since the last consolidation / live then
+  int64_t deleted_at_consolidation = 0;
+  int64_t consolidations = 0;
   int last_launches = 0;                // kernels launched by the last run_search
   int ho_pct = -1;                      // pair-mode handoff threshold (% of one-warp warps): -1 auto, 0 off
   unsigned long long* ho = nullptr;     // handoff control words + slots of svf_search (handoff_words(), lazy)
@@ -605,6 +608,8 @@ svf_status svf_insert(svf_index* idx, const float* X, int64_t n, uint32_t* out_i
   return SVF_OK;
 }
 
+static svf_status consolidate_impl(svf_index* idx, int64_t* n_rewritten, cudaStream_t st);
+
 svf_status svf_delete(svf_index* idx, const uint32_t* ids, int64_t n, int64_t* n_newly_deleted, void* stream) {
   svf_status s = enter(idx);
   if (s != SVF_OK) return s;
@@ -635,6 +640,12 @@ svf_status svf_delete(svf_index* idx, const uint32_t* ids, int64_t n, int64_t* n
   CK(idx, cudaStreamSynchronize(st), "delete sync");
   idx->n_deleted += (int64_t)hn;
   if (n_newly_deleted) *n_newly_deleted = (int64_t)hn;
+  // NEXT-4: global consolidation once the deletions since the last one pass the ratio ("e.g., 20%")
+  if (idx->consolidate_ratio > 0.0) {
+    const int64_t since = idx->n_deleted - idx->deleted_at_consolidation;
+    const int64_t base = idx->n_alloc - idx->deleted_at_consolidation;
+    if (since > 0 && (double)since > idx->consolidate_ratio * (double)base) return consolidate_impl(idx, nullptr, st);
+  }
   return SVF_OK;
 }
 
@@ -799,15 +810,8 @@ svf_status svf_read_trace(svf_index* idx, uint64_t* out, int64_t cap, int64_t* n
   return SVF_OK;
 }
 
-svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
-                      void* stream) {
-  svf_status s = enter(idx);
-  if (s != SVF_OK) return s;
-  if (c < 1 || c > 32 || !(threshold >= 0.0 && threshold < 1.0))
-    return fail(SVF_ERR_INVALID, "need 1 <= c <= 32 and 0 <= threshold < 1");
-  std::lock_guard<std::mutex> lk(idx->mu);
-  DeviceGuard g(idx->dev);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+// NEXT-1 repair / NEXT-4 consolidation on the update path (caller holds the index lock)
+static svf_status repair_impl(svf_index* idx, int c, double threshold, int64_t* n_repaired, uint64_t* hist, cudaStream_t st) {
   const uint32_t* tomb = idx->n_deleted > 0 ? idx->tomb : nullptr;
   CK(idx, ensure_scratch(idx, repair_mark_scratch_bytes(idx->n_alloc), st), "repair scratch");
   int64_t n_list = 0;
@@ -829,6 +833,53 @@ svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_re
   if (n_repaired) *n_repaired = n_list;
   if (hist)
     for (int i = 0; i < 5; ++i) hist[i] = h[i];
+  return SVF_OK;
+}
+
+svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
+                      void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (c < 1 || c > idx->R || !(threshold >= 0.0 && threshold < 1.0))
+    return fail(SVF_ERR_INVALID, "need 1 <= c <= degree and 0 <= threshold < 1");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  return repair_impl(idx, c, threshold, n_repaired, hist, static_cast<cudaStream_t>(stream));
+}
+
+// NEXT-4 global consolidation: every live vertex with a deleted neighbour p gets all live members of
+// N_out(p) as candidates (repair with c = R and threshold 0, reading C1 in DESIGN.md)
+static svf_status consolidate_impl(svf_index* idx, int64_t* n_rewritten, cudaStream_t st) {
+  svf_status s = repair_impl(idx, idx->R, 0.0, n_rewritten, nullptr, st);
+  if (s != SVF_OK) return s;
+  idx->deleted_at_consolidation = idx->n_deleted;
+  idx->consolidations++;
+  return SVF_OK;
+}
+
+svf_status svf_consolidate(svf_index* idx, int64_t* n_rewritten, void* stream) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  DeviceGuard g(idx->dev);
+  return consolidate_impl(idx, n_rewritten, static_cast<cudaStream_t>(stream));
+}
+
+svf_status svf_set_consolidation(svf_index* idx, double ratio) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  if (!(ratio >= 0.0 && ratio < 1.0)) return fail(SVF_ERR_INVALID, "consolidation ratio must be in [0, 1)");
+  std::lock_guard<std::mutex> lk(idx->mu);
+  idx->consolidate_ratio = ratio;
+  return SVF_OK;
+}
+
+svf_status svf_consolidation_stats(svf_index* idx, int64_t out[2]) {
+  svf_status s = enter(idx);
+  if (s != SVF_OK) return s;
+  std::lock_guard<std::mutex> lk(idx->mu);
+  out[0] = idx->consolidations;
+  out[1] = idx->deleted_at_consolidation;
   return SVF_OK;
 }
 

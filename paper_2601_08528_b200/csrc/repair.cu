@@ -9,6 +9,8 @@
 //                        (dist, id) -> a candidate list exactly like an insertion's;
 //   K-L1 detour select   the insertion's neighbour selection over U into staged rows;
 //   repair_scatter       staged rows -> graph / edge_dist.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -61,21 +63,26 @@ __device__ __forceinline__ void set_put(uint32_t* tab, int bits, uint32_t id) {
   while (atomicCAS(tab + h, kSent, id) != kSent && tab[h] != id) h = (h + 1) & mask;
 }
 
-// ER = registers per lane for a row (R <= 32*ER); EU = registers for the union's cap (cap <= 32*EU)
+// ER = registers per lane for a row (R <= 32*ER); EU = registers for the union's cap (cap <= 32*EU).
+// Candidates are gathered in chunks of at most buf_cap (>= 2R) ids: a chunk is scored and merged into the running
+// top-cap list whenever another deleted neighbour's row might not fit, so c may be as large as R (consolidation:
+// every live member of every deleted neighbour's row) with a chunk buffer of 2R ids.  The union's cap smallest keys
+// do not depend on the chunking (keys are distinct).
 template <int ER, int EU>
 __global__ void __launch_bounds__(kRepWarps * 32)
     repair_union_kernel(const uint32_t* __restrict__ graph, const float* __restrict__ edge_dist,
                         const float* __restrict__ vec, int dq, int metric, const uint32_t* __restrict__ tomb, int R,
-                        int c, int cap, const uint32_t* __restrict__ list, int64_t n_list, int set_bits, int cand_cap,
+                        int c, int cap, const uint32_t* __restrict__ list, int64_t n_list, int set_bits, int buf_cap,
                         uint32_t* __restrict__ u_ids, float* __restrict__ u_d) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)cand_cap * 4 + (size_t)cand_cap * 8 + 15) & ~(size_t)15;
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)buf_cap * 4 + (size_t)buf_cap * 8 + 15) & ~(size_t)15;
   unsigned char* base = smem + per_warp * wib;
   uint32_t* tab = reinterpret_cast<uint32_t*>(base);
   uint32_t* cid = tab + (1 << set_bits);
-  uint64_t* ckey = reinterpret_cast<uint64_t*>(cid + cand_cap);
-  for (int64_t w = (int64_t)blockIdx.x * kRepWarps + wib; w < n_list; w += (int64_t)gridDim.x * kRepWarps) {
+  uint64_t* ckey = reinterpret_cast<uint64_t*>(cid + buf_cap);
+  const int wpb = blockDim.x >> 5;
+  for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < n_list; w += (int64_t)gridDim.x * wpb) {
     const uint32_t v = list[w];
     for (int i = lane; i < (1 << set_bits); i += 32) tab[i] = kSent;
     __syncwarp();
@@ -92,13 +99,48 @@ __global__ void __launch_bounds__(kRepWarps * 32)
       if (live) set_put(tab, set_bits, rid[r]);
     }
     __syncwarp();
-    // candidates: deleted p in slot order, first c qualifying members of N_out(p) in slot order
+    warp_sort<EU>(best, lane);
+    const float4* xv = reinterpret_cast<const float4*>(vec) + (size_t)v * dq;
     int ncand = 0;
+    // score the buffered candidates (a lane per candidate, rows read as float4) and merge them into best
+    auto flush = [&]() {
+      for (int i = lane; i < ncand; i += 32) {
+        const float4* xc = reinterpret_cast<const float4*>(vec) + (size_t)cid[i] * dq;
+        float acc = 0.f;
+        for (int j = 0; j < dq; ++j) {
+          const float4 a = __ldg(xv + j), b = __ldg(xc + j);
+          if (metric == 0) {
+            const float d0 = b.x - a.x, d1 = b.y - a.y, d2 = b.z - a.z, d3 = b.w - a.w;
+            acc = fmaf(d0, d0, acc);
+            acc = fmaf(d1, d1, acc);
+            acc = fmaf(d2, d2, acc);
+            acc = fmaf(d3, d3, acc);
+          } else {
+            acc = fmaf(b.x, a.x, acc);
+            acc = fmaf(b.y, a.y, acc);
+            acc = fmaf(b.z, a.z, acc);
+            acc = fmaf(b.w, a.w, acc);
+          }
+        }
+        ckey[i] = make_key((metric == 0 ? acc : -acc) + 0.0f, cid[i]);
+      }
+      __syncwarp();
+      for (int c0 = 0; c0 < ncand; c0 += 32) {
+        uint64_t cc[1];
+        cc[0] = c0 + lane < ncand ? ckey[c0 + lane] : kEmptyKey;
+        warp_sort<1>(cc, lane);
+        warp_merge_into<EU, 1>(best, cc, lane);
+      }
+      __syncwarp();
+      ncand = 0;
+    };
+    // candidates: deleted p in slot order, first c qualifying members of N_out(p) in slot order
 #pragma unroll
     for (int r = 0; r < ER; ++r) {
       for (int l = 0; l < 32; ++l) {
         const uint32_t p = __shfl_sync(0xffffffffu, rid[r], l);
         if (r * 32 + l >= R || p == kSent || !tomb_dead(tomb, p)) continue;
+        if (ncand + min(c, R) > buf_cap) flush();
         int got = 0;
 #pragma unroll
         for (int r2 = 0; r2 < ER; ++r2) {
@@ -107,47 +149,18 @@ __global__ void __launch_bounds__(kRepWarps * 32)
           const bool ok = x != kSent && x != v && !tomb_dead(tomb, x) && !set_has(tab, set_bits, x);
           const unsigned m = __ballot_sync(0xffffffffu, ok);
           const int rank = got + __popc(m & ((1u << lane) - 1u));
-          const bool take = ok && rank < c && ncand + rank < cand_cap;
+          const bool take = ok && rank < c;
           if (take) {
             cid[ncand + rank] = x;
             set_put(tab, set_bits, x);
           }
           got = min(got + __popc(m), c);
         }
-        ncand = min(ncand + got, cand_cap);
+        ncand += got;
         __syncwarp();
       }
     }
-    // fresh distances of the candidates to v (a lane per candidate, rows read as float4)
-    const float4* xv = reinterpret_cast<const float4*>(vec) + (size_t)v * dq;
-    for (int i = lane; i < ncand; i += 32) {
-      const float4* xc = reinterpret_cast<const float4*>(vec) + (size_t)cid[i] * dq;
-      float acc = 0.f;
-      for (int j = 0; j < dq; ++j) {
-        const float4 a = __ldg(xv + j), b = __ldg(xc + j);
-        if (metric == 0) {
-          const float d0 = b.x - a.x, d1 = b.y - a.y, d2 = b.z - a.z, d3 = b.w - a.w;
-          acc = fmaf(d0, d0, acc);
-          acc = fmaf(d1, d1, acc);
-          acc = fmaf(d2, d2, acc);
-          acc = fmaf(d3, d3, acc);
-        } else {
-          acc = fmaf(b.x, a.x, acc);
-          acc = fmaf(b.y, a.y, acc);
-          acc = fmaf(b.z, a.z, acc);
-          acc = fmaf(b.w, a.w, acc);
-        }
-      }
-      ckey[i] = make_key((metric == 0 ? acc : -acc) + 0.0f, cid[i]);
-    }
-    __syncwarp();
-    warp_sort<EU>(best, lane);
-    for (int c0 = 0; c0 < ncand; c0 += 32) {
-      uint64_t cc[1];
-      cc[0] = c0 + lane < ncand ? ckey[c0 + lane] : kEmptyKey;
-      warp_sort<1>(cc, lane);
-      warp_merge_into<EU, 1>(best, cc, lane);
-    }
+    flush();
 #pragma unroll
     for (int r = 0; r < EU; ++r) {
       const int s = r * 32 + lane;
@@ -215,16 +228,20 @@ cudaError_t launch_repair_apply(uint32_t* graph, float* edge_dist, const float* 
   uint32_t* rows = reinterpret_cast<uint32_t*>(sp);
   sp += al256((size_t)n_list * R * 4);
   float* rows_d = reinterpret_cast<float*>(sp);
-  const int cand_cap = c * R;
+  // visited set for the row and every candidate (load <= 1/2; <= 2^13 slots: load <= 0.51 at c = R = 64)
+  const int cand_total = std::min(c, R) * R;
   int set_bits = 1;
-  while ((1 << set_bits) < 2 * (R + cand_cap)) ++set_bits;
-  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)cand_cap * 12 + 15) & ~(size_t)15;
-  const size_t smem = per_warp * kRepWarps;
+  while ((1 << set_bits) < 2 * (R + cand_total) && set_bits < 13) ++set_bits;
+  while ((1 << set_bits) < (R + cand_total) * 5 / 4) ++set_bits;  // large sets: load <= 0.8
+  const int buf_cap = 2 * R;                           // chunk buffer: room for one more deleted neighbour's row
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)buf_cap * 12 + 15) & ~(size_t)15;
+  const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kRepWarps, (200u << 10) / per_warp));
+  const size_t smem = per_warp * wpb;
   auto run = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
-    kern<<<(unsigned)(num_sms * 8), kRepWarps * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, c, cap,
-                                                                list, n_list, set_bits, cand_cap, u_ids, u_d);
+    kern<<<(unsigned)(num_sms * 8), wpb * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, c, cap,
+                                                                list, n_list, set_bits, buf_cap, u_ids, u_d);
     return cudaGetLastError();
   };
   cudaError_t e;

@@ -401,3 +401,45 @@ def test_search_overlapping_insert_on_two_streams(svf, c1):
     ri, rd, _ = oracle.graph_search(st["vec"], st["graph"], Qb, 10, 32)
     ids2, d2 = idx.search(Qd, 10, 32)
     assert np.array_equal(u32(ids2), ri) and np.array_equal(f32(d2), rd)
+
+
+@pytest.mark.parametrize("R,frac", [(32, 0.25), (64, 0.3), (16, 0.6)])
+def test_consolidate_bit_exact(svf, R, frac):
+    """NEXT-4 global consolidation (svf_consolidate) equals oracle.consolidate bit for bit (rows and
+    edge distances, integer data), incl. degree 64 (c = 64: the chunked candidate union with a 2^13-slot set)."""
+    X = GLM(dim=32, ell=8, integer=True).rows(5, 5, 0, 5000)
+    G, E = oracle.build(X, R=R, seed_size=600, B_ins=500, L_ins=128)
+    dead = random_tombstones(5000, frac, seed=R)
+    tomb = pack_tomb(dead, 5000)
+    idx = svf.Index.from_state(X, G, E, tomb=tomb)
+    n = idx.consolidate()
+    st = idx.export()
+    g2, e2, n2 = oracle.consolidate(X, G, E, tomb)
+    assert n == n2 > 0
+    assert np.array_equal(st["graph"], g2) and np.array_equal(st["edge_dist"], e2)
+    live = np.setdiff1d(np.arange(5000), dead)
+    assert not np.isin(st["graph"][live], dead).any()
+
+
+def test_consolidation_triggers_after_deletion_ratio(svf, c1):
+    """svf_set_consolidation(0.2): a delete of 15% does not trigger it, a further 10% (25% since the last
+    consolidation) does, on the delete call; the result equals the oracle's consolidation of the final tombstones,
+    and searches after it match the oracle on the consolidated graph."""
+    X, Q, g, e = c1
+    idx = svf.Index.from_state(X, g, e)
+    idx.set_consolidation(0.2)
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(len(X)).astype(np.uint32)
+    d1, d2 = perm[:1500], perm[1500:2500]
+    idx.delete(cuda(d1.astype(np.int32)))
+    assert idx.consolidation_stats()["consolidations"] == 0
+    idx.delete(cuda(d2.astype(np.int32)))
+    stats = idx.consolidation_stats()
+    assert stats["consolidations"] == 1 and stats["deleted_at_last"] == 2500
+    tomb = pack_tomb(perm[:2500], len(X))
+    g2, e2, _ = oracle.consolidate(X, g, e, tomb)
+    st = idx.export()
+    assert np.array_equal(st["graph"], g2) and np.array_equal(st["edge_dist"], e2)
+    ids, d = idx.search(cuda(Q), 10, 32)
+    ri, rd, _ = oracle.graph_search(X, g2, Q, 10, 32, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)

@@ -459,3 +459,56 @@ def test_repair_properties_on_a_built_graph(orc):
             if x not in allowed:
                 assert any(x in lst for lst in per_p.values())       # replacements come from N_out(p)
         assert len(set(new) - allowed) <= c * len(per_p)            # O(cR) added edges
+
+
+# ---- NEXT-4 global consolidation (reading C1) -------------------------------------------------------
+def test_consolidate_hand_example(orc):
+    """Points 0,1,2,3,4,10 on a line (D=4, zero-padded), R=2, P=1; vertex 2 deleted.  By hand: the live rows
+    holding 2 are 0, 1 and 3.  Row 0: live {1 (d 1)} + N_out(2) = {1, 3} minus taken/self -> 3 (d 9); detour
+    counts on the starting rows are 0 and 0 -> [1 | 3].  Row 1: {0 (1)} + {3 (4)} (1 itself skipped) -> [0 | 3].
+    Row 3: {4 (1)} + {1 (4)} (3 itself skipped) -> [4 | 1].  Rows 2 (deleted), 4 and 5 are untouched."""
+    xs = [0, 1, 2, 3, 4, 10]
+    X = np.zeros((6, 4), np.float32)
+    X[:, 0] = xs
+    G = np.array([[1, 2], [2, 0], [1, 3], [2, 4], [3, 5], [4, 3]], np.uint32)
+    E = np.array([[(xs[v] - xs[u]) ** 2 for u in G[v]] for v in range(6)], np.float32)
+    tomb = pack_tomb(np.array([2], np.uint32), 6)
+    g2, e2, n = orc.consolidate(X, G, E, tomb, P=1)
+    assert n == 3
+    exp_g = np.array([[1, 3], [0, 3], [1, 3], [4, 1], [3, 5], [4, 3]], np.uint32)
+    exp_e = np.array([[1, 9], [1, 4], E[2], [1, 4], E[4], E[5]], np.float32)
+    assert np.array_equal(g2, exp_g) and np.array_equal(e2, exp_e)
+
+
+def test_consolidate_properties_on_a_built_graph(orc):
+    """After consolidation no live row references a deleted vertex (the defining effect: all affected
+    neighbourhoods); only rows that held a deleted id change; new entries come from the row itself or from the
+    deleted neighbours' lists; deleted rows are frozen; every row keeps the prefix/tail layout."""
+    X = GLM(dim=16, ell=6, integer=True).rows(8, 8, 0, 3000)
+    R = 16
+    G, E = orc.build(X, R=R, seed_size=500, B_ins=400, L_ins=48)
+    dead = random_tombstones(3000, 0.25, seed=11)
+    tomb = pack_tomb(dead, 3000)
+    deadset = set(dead.tolist())
+    g2, e2, n = orc.consolidate(X, G, E, tomb)
+    live = np.setdiff1d(np.arange(3000), dead)
+    assert not np.isin(g2[live], dead).any()
+    affected = [v for v in live if any(int(x) in deadset for x in G[v] if x != SENT)]
+    assert n == len(affected) > 0
+    assert np.array_equal(g2[dead], G[dead])
+    unaff = np.setdiff1d(live, affected)
+    assert np.array_equal(g2[unaff], G[unaff])
+    for v in affected[:300]:
+        old = [int(x) for x in G[v] if x != SENT]
+        pool = set(x for x in old if x not in deadset)
+        for p in old:
+            if p in deadset:
+                pool |= set(int(x) for x in G[p] if x != SENT and int(x) not in deadset and int(x) != v)
+        new = [int(x) for x in g2[v] if x != SENT]
+        assert set(new) <= pool and v not in new and len(set(new)) == len(new)
+        assert len(new) == min(R, len(pool))
+        tail = [(float(e2[v, s]), int(g2[v, s])) for s in range(R // 2, R) if g2[v, s] != SENT]
+        assert tail == sorted(tail)
+    # consolidation equals repair with every deleted neighbour's whole list at threshold 0
+    g3, e3, n3, _ = orc.repair(X, G, E, tomb, c=R, threshold=0.0)
+    assert np.array_equal(g2, g3) and np.array_equal(e2, e3) and n3 == n

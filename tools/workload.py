@@ -1,7 +1,8 @@
 """Replay a paper-style streaming trace (workloads/traces.py) on the GPU index and report recall@10 against exact
 ground truth over the live set, search QPS, insert and delete rates per evaluated step.
 
-  python tools/workload.py --trace expiration --config C2 --n 1000000 --itopk 32 [--repair 0.15] --out f.json
+  python tools/workload.py --trace expiration --config C2 --n 1000000 --itopk 32 [--repair 0.15] [--consolidate 0.2]
+      --out f.json
 """
 import argparse
 import json
@@ -27,6 +28,8 @@ def main():
     ap.add_argument("--t-max", type=int, default=200)
     ap.add_argument("--itopk", type=int, default=32)
     ap.add_argument("--repair", type=float, default=0.0, help="repair threshold after each delete (0 = off)")
+    ap.add_argument("--consolidate", type=float, default=0.0,
+                    help="automatic global consolidation ratio (svf_set_consolidation; 0 = off, paper: 0.2)")
     ap.add_argument("--max-evals", type=int, default=12)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -56,6 +59,8 @@ def main():
         if len(ins):
             if idx is None:
                 idx = svf.Index.build(Xd[ins], degree=c["degree"], metric=c["metric"], capacity=a.n + 1)
+                if a.consolidate > 0:
+                    idx.set_consolidation(a.consolidate)
                 new = np.arange(len(ins))
             else:
                 e0, e1 = ev()
@@ -93,6 +98,7 @@ def main():
             evals.append(r)
             print(json.dumps(r), flush=True)
     summ = {"trace": a.trace, "config": a.config, "n": a.n, "itopk": a.itopk, "repair": a.repair,
+            "consolidate": a.consolidate, "consolidations": idx.consolidation_stats()["consolidations"],
             "steps": len(steps), "wall_s": round(time.time() - t_start, 1),
             "inserts_per_s": round(sum(n for n, _ in t_ins) / max(1e-9, sum(t for _, t in t_ins) / 1e3)),
             "deletes_per_s": round(sum(n for n, _ in t_del) / max(1e-9, sum(t for _, t in t_del) / 1e3)),
