@@ -8,8 +8,10 @@
 //   warp 1      TMEM owner (512 columns = 2 accumulators of 128 lanes x 256 fp32) and single-thread MMA issuer:
 //               4 x tcgen05.mma.kind::tf32 (M=128, N=256, K=8) per 32-float chunk; tcgen05.commit frees the stage
 //               and, after the last chunk, publishes the accumulator;
-//   warps 2..5  epilogue: thread = query row = TMEM lane; tcgen05.ld 32 columns at a time, approximate score
-//               s~ = ||x||^2 - 2 q.x (L2) or -q.x (IP), keep the 32 smallest per (query, split) in registers.
+//   warps 2..9  epilogue: thread = query row = TMEM lane; tcgen05.ld 32 columns at a time of the approximate
+//               score s~ = ||x||^2 - 2 q.x (L2) or -q.x (IP), which the MMA produces directly: A rows are
+//               [-2q | 0 | w] and B rows [x | 0 | p] with ||x||^2 = w.p split into pieces exact in TF32, one extra
+//               K=8 MMA per tile; the epilogue keeps the KL smallest per (query, split, column half) in registers.
 // knn_rerank_kernel (warp per query): merge the per-split lists to the best 64 approximate candidates, recompute
 //   their distances exactly (direct-difference FFMA, the search kernel's arithmetic), sort, emit the top k, and
 //   check the certificate  d_k < tau - E + ||q||^2  (tau = smallest score any excluded row can have, E = the
@@ -128,23 +130,27 @@ struct TcArgs {
   int stages;            // B ring depth
   int64_t rows_per_split;
   int64_t splits, units; // units = qtiles * splits
-  const float* norms;    // ||x||^2 per row (L2); unused for IP
+  const float* unused_norms;
   const uint32_t* tomb;
   int64_t self_base;     // >= 0: exclude id == self_base + query
   int metric;
   uint64_t* cand;        // [splits*2][nq][KL] keys (approx score, id), sorted ascending
+  int has_norm;          // L2: one more B chunk (the norm pieces) and one more K=8 MMA per tile
+  const float* thr0;     // nullable: per-query pruning threshold in score space (from a sample pass)
 };
 
 // KL = per-thread (query row, split, column half) list length: 16 when k <= 16, else 32
 template <bool kTomb, bool kSelf, int KL>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    knn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap xmap, TcArgs a) {
+    knn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap xmap,
+                  const __grid_constant__ CUtensorMap nmap, TcArgs a) {
   constexpr int TC_LIST = KL;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned operand area (SWIZZLE_128B atoms)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  unsigned char* sA = smem;                                   // kc x 16 KB
-  unsigned char* sB = sA + (size_t)a.kc * kAChunkBytes;       // stages x 32 KB
+  const int kca = a.kc + (a.has_norm ? 1 : 0);                // A chunks: the query tile + the norm weights
+  unsigned char* sA = smem;                                   // kca x 16 KB
+  unsigned char* sB = sA + (size_t)kca * kAChunkBytes;        // stages x 32 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)a.stages * kBStageBytes);
   uint64_t* full = bars;                   // [stages]
   uint64_t* empty = full + a.stages;       // [stages]
@@ -153,7 +159,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* t_full = a_empty + 1;          // [2]
   uint64_t* t_empty = t_full + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
-  float* wnorm_all = reinterpret_cast<float*>(bars + 64);  // [kTcEpiWarps][32], 16-byte aligned (bars area 512 B)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -170,6 +175,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    if (a.has_norm) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&nmap)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -189,14 +195,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int64_t r0 = sp * a.rows_per_split, r1 = min(a.n, r0 + a.rows_per_split);
         mbar_wait(a_empty, aphase ^ 1);
         aphase ^= 1;
-        mbar_expect_tx(a_full, (uint32_t)a.kc * kAChunkBytes);
-        for (int c = 0; c < a.kc; ++c)
+        mbar_expect_tx(a_full, (uint32_t)kca * kAChunkBytes);
+        for (int c = 0; c < kca; ++c)
           tma_load_2d(sA + (size_t)c * kAChunkBytes, &qmap, a_full, c * TC_KC, (int)(qt * TC_M));
         for (int64_t nb = r0; nb < r1; nb += TC_N) {
-          for (int c = 0; c < a.kc; ++c) {
+          for (int c = 0; c < kca; ++c) {
             mbar_wait(empty + stage, phase ^ 1);
             mbar_expect_tx(full + stage, kBStageBytes);
-            tma_load_2d(sB + (size_t)stage * kBStageBytes, &xmap, full + stage, c * TC_KC, (int)nb);
+            if (c < a.kc)
+              tma_load_2d(sB + (size_t)stage * kBStageBytes, &xmap, full + stage, c * TC_KC, (int)nb);
+            else  // the norm pieces of the same 256 rows
+              tma_load_2d(sB + (size_t)stage * kBStageBytes, &nmap, full + stage, 0, (int)nb);
             if (++stage == (uint32_t)a.stages) {
               stage = 0;
               phase ^= 1;
@@ -218,14 +227,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tphase[acc] ^= 1;
           tc_fence_after();
           const uint32_t d = tmem_base + acc * TC_N;
-          for (int c = 0; c < a.kc; ++c) {
+          for (int c = 0; c < kca; ++c) {
             mbar_wait(full + stage, phase);
             tc_fence_after();
             const uint32_t abase = smem_u32(sA + (size_t)c * kAChunkBytes);
             const uint32_t bbase = smem_u32(sB + (size_t)stage * kBStageBytes);
+            if (c < a.kc) {
 #pragma unroll
-            for (int kk = 0; kk < TC_KC / 8; ++kk)  // K = 8 tf32 (32 bytes) per MMA
-              umma_tf32(d, sdesc(abase + kk * 32), sdesc(bbase + kk * 32), (c | kk) ? 1u : 0u);
+              for (int kk = 0; kk < TC_KC / 8; ++kk)  // K = 8 tf32 (32 bytes) per MMA
+                umma_tf32(d, sdesc(abase + kk * 32), sdesc(bbase + kk * 32), (c | kk) ? 1u : 0u);
+            } else {
+              umma_tf32(d, sdesc(abase), sdesc(bbase), 1u);  // + w . p = ||x||^2 (the pieces sit in K = 0..2)
+            }
             umma_commit(empty + stage);
             if (++stage == (uint32_t)a.stages) {
               stage = 0;
@@ -239,7 +252,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {  // ---------------- epilogue: thread = query row = TMEM lane, half of the 256 columns ----------------
-    float* wnorm = wnorm_all + (warp - 2) * 32;
     const int lq = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;        // columns [half*128, half*128+128) of every tile
     const int row = lq * 32 + lane;
@@ -255,7 +267,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         bv[i] = __int_as_float(0x7F800000);
         bi[i] = kSent;
       }
-      float thr = bv[TC_LIST - 1];
+      // rows scoring >= thr0 cannot be among the query's k nearest (a sample already holds k rows below it), so
+      // the lists start with that bound: far fewer (warp-divergent) insertions
+      const float thr0 = (a.thr0 != nullptr && qi < a.nq) ? a.thr0[qi] : __int_as_float(0x7F800000);
+      float thr = fminf(bv[TC_LIST - 1], thr0);
       for (int64_t nb = r0; nb < r1; nb += TC_N) {
         mbar_wait(t_full + acc, tphase[acc]);
         tphase[acc] ^= 1;
@@ -269,14 +284,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           continue;
         }
 #endif
-        // one 32-column chunk: scores, their minimum over 4 independent chains, and (rarely) insertions
+        // one 32-column chunk: the MMA's scores, their minimum over 4 independent chains, (rarely) insertions
         auto process = [&](uint32_t(&v)[32], int c0) {
           const int64_t cb = nb + half * (TC_N / 2) + c0;
-          // this chunk's 32 norms, staged per warp for broadcast float4 reads (+inf outside the split)
-          __syncwarp();
-          wnorm[lane] = (cb + lane < r1) ? (a.metric == 0 ? __ldg(a.norms + cb + lane) : 0.f)
-                                         : __int_as_float(0x7F800000);
-          __syncwarp();
           // valid columns: inside the split, not deleted, not the query itself
           uint32_t valid = cb >= r1 ? 0u : (r1 - cb >= 32 ? 0xFFFFFFFFu : ((1u << (uint32_t)(r1 - cb)) - 1u));
           if (kTomb && cb < r1) valid &= ~__ldg(a.tomb + (cb >> 5));
@@ -287,21 +297,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           float mn4[4] = {__int_as_float(0x7F800000), __int_as_float(0x7F800000), __int_as_float(0x7F800000),
                           __int_as_float(0x7F800000)};
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 n4 = reinterpret_cast<const float4*>(wnorm)[j4];
-            const float nj[4] = {n4.x, n4.y, n4.z, n4.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int j = j4 * 4 + t;
-              const float dot = __uint_as_float(v[j]);
-              const float sc = a.metric == 0 ? fmaf(-2.f, dot, nj[t]) : (nj[t] == 0.f ? -dot : nj[t]);
-              v[j] = __float_as_uint(sc);
-              mn4[t] = fminf(mn4[t], sc);
-            }
-          }
+          for (int j = 0; j < 32; ++j) mn4[j & 3] = fminf(mn4[j & 3], __uint_as_float(v[j]));
           const float mn = fminf(fminf(mn4[0], mn4[1]), fminf(mn4[2], mn4[3]));
           uint32_t pass = 0;
-          if (mn < thr) {
+          if (mn < thr && valid != 0u) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(v[j]) < thr ? 1u : 0u) << j;
             pass &= valid;
@@ -327,7 +326,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               }
             }
           }
-          thr = bv[TC_LIST - 1];
+          thr = fminf(bv[TC_LIST - 1], thr0);
         };
         // software pipeline over the 4 chunks: the next chunk's TMEM load is in flight while one is processed
         uint32_t va[32], vb[32];
@@ -362,27 +361,99 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
-// ||x||^2 per row (fp32 FFMA) + dataset facts for the TF32 error bound: max ||x||, all values integer <= 2047
-__global__ void row_norms_kernel(const float* __restrict__ vec, int dp, int64_t n, float* __restrict__ norms,
+// ||x||^2 per row (fp32 FFMA) as the B operand's extra K chunk: pieces hi, mid, lo, each exact in TF32 (the top
+// 11 significant bits of what remains), so that hi + mid + lo = ||x||^2 up to 2^-35 relative (exactly for integer
+// norms < 2^24); plus dataset facts for the TF32 error bound: max ||x||, all values integer <= 2047
+__global__ void row_norms_kernel(const float* __restrict__ vec, int dp, int64_t n, float* __restrict__ npieces,
                                  unsigned int* __restrict__ facts) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= n) return;
-  float acc = 0.f;
-  bool integral = true;
-  for (int c = lane; c < dp; c += 32) {
-    const float x = __ldg(vec + r * dp + c);
-    acc = fmaf(x, x, acc);
-    integral = integral && (x == rintf(x)) && fabsf(x) <= 2047.f;
-  }
+  // grid-stride over rows, warp per row; the facts are reduced per warp and per block before one atomic per
+  // block (a global atomic per row serialised on one address: 0.75 ms at 1M rows)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ unsigned int s_max[32], s_int[32];
+  unsigned int wmax = 0u;
+  bool wint = true;
+  for (int64_t r = (int64_t)blockIdx.x * nw + wib; r < n; r += (int64_t)gridDim.x * nw) {
+    float acc = 0.f;
+    bool integral = true;
+    for (int c = lane; c < dp; c += 32) {
+      const float x = __ldg(vec + r * dp + c);
+      acc = fmaf(x, x, acc);
+      integral = integral && (x == rintf(x)) && fabsf(x) <= 2047.f;
+    }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  const bool all_int = __all_sync(0xffffffffu, integral);
-  if (lane == 0) {
-    norms[r] = acc;
-    atomicMax(facts + 0, __float_as_uint(sqrtf(acc)));  // positive floats order like their bit patterns
-    if (!all_int) atomicAnd(facts + 1, 0u);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    wint = wint && __all_sync(0xffffffffu, integral);
+    const float hi = __uint_as_float(__float_as_uint(acc) & 0xFFFFE000u);
+    const float rem = acc - hi;  // exact (Sterbenz)
+    const float mid = __uint_as_float(__float_as_uint(rem) & 0xFFFFE000u);
+    const float lo = __uint_as_float(__float_as_uint(rem - mid) & 0xFFFFE000u);
+    npieces[r * 32 + lane] = lane == 0 ? hi : (lane == 1 ? mid : (lane == 2 ? lo : 0.f));
+    wmax = max(wmax, __float_as_uint(sqrtf(acc)));  // positive floats order like their bit patterns
   }
+  if (lane == 0) {
+    s_max[wib] = wmax;
+    s_int[wib] = wint ? 1u : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int m = 0u, in = 1u;
+    for (int w = 0; w < nw; ++w) {
+      m = max(m, s_max[w]);
+      in &= s_int[w];
+    }
+    atomicMax(facts + 0, m);
+    if (!in) atomicAnd(facts + 1, 0u);
+  }
+}
+
+// Pruning threshold per query from the exact k-th distance d_s among a row sample (a valid upper bound of the
+// true k-th): in score space (L2: s = d - ||q||^2, IP: s = d), raised by the TF32 error bound 2E of the
+// approximate scores and a relative/absolute slack, so that every row of the true top k scores strictly below it.
+__global__ void prune_threshold_kernel(const float* __restrict__ Q, int64_t q_stride, int q_dim, int64_t nq, int k,
+                                       const float* __restrict__ d_sample, int metric, int D,
+                                       const unsigned int* __restrict__ facts, float* __restrict__ thr0) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  const float ds = d_sample[qi * k + k - 1];
+  if (!(ds < __int_as_float(0x7F800000))) {
+    thr0[qi] = __int_as_float(0x7F800000);
+    return;
+  }
+  double qn = 0.0;
+  bool qint = true;
+  for (int c = 0; c < q_dim; ++c) {
+    const float x = Q[(size_t)qi * q_stride + c];
+    qn += (double)x * x;
+    qint = qint && x == rintf(x) && fabsf(x) <= 2047.f;
+  }
+  const double xmax = (double)__uint_as_float(facts[0]);
+  const double qnorm = sqrt(qn);
+  // integer data (the K-R exactness condition): scores are exact integers, so +1 keeps the true top k strictly
+  // below; otherwise the TF32 bound 2E plus the fp32 rounding of d_s and ||q||^2
+  const bool exact = facts[1] != 0u && qint && xmax * xmax + 2.0 * qnorm * xmax < 16777216.0;
+  const double u = 1.0 / 512.0 + (D + 9) * 2.384185791015625e-07;
+  const double E = exact ? 0.0
+                         : (metric == 0 ? 2.0 : 1.0) * u * qnorm * xmax +
+                               (D + 4) * 5.9604644775390625e-08 * (xmax * xmax + qn);
+  const double sc = (double)ds - (metric == 0 ? qn : 0.0);
+  const double slack = (D + 4) * 1.1920928955078125e-07 * (fabs((double)ds) + qn) + (exact ? 1.0 : 1e-30);
+  const double t = sc + 2.0 * E + slack;
+  thr0[qi] = __double2float_ru(t + 1e-6 * fabs(t));  // rounded up: the bound never tightens
+}
+
+// A operand rows [s*q | 0 | w]: s = -2 (L2) or -1 (IP), exact in TF32 for the integer queries the exactness
+// argument covers; w = (1, 1, 1) picks up the norm pieces (L2 only).  Row length (kc + 1) * 32 floats.
+__global__ void stage_queries_kernel(const float* __restrict__ Q, int64_t q_stride, int q_dim, int64_t nq, int kc,
+                                     int metric, float* __restrict__ qa) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = (kc + 1) * 32;
+  if (t >= nq * w) return;
+  const int64_t r = t / w;
+  const int c = (int)(t - r * w);
+  float v = 0.f;
+  if (c < q_dim) v = (metric == 0 ? -2.f : -1.f) * Q[(size_t)r * q_stride + c];
+  else if (c >= kc * 32 && c < kc * 32 + 3 && metric == 0) v = 1.f;
+  qa[t] = v;
 }
 
 // K-R: exact re-rank of the approximate candidates + certificate (warp per query)
@@ -391,7 +462,8 @@ __global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t spl
                                   const float* __restrict__ vec, int dq, const float* __restrict__ Q,
                                   int64_t q_stride, int q_dim, int metric, const unsigned int* __restrict__ facts,
                                   uint32_t* __restrict__ out_ids, float* __restrict__ out_d,
-                                  uint32_t* __restrict__ fail_list, unsigned int* __restrict__ n_fail) {
+                                  uint32_t* __restrict__ fail_list, unsigned int* __restrict__ n_fail,
+                                  const float* __restrict__ thr0) {
   const int lane = threadIdx.x & 31;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (qi >= nq) return;
@@ -407,6 +479,7 @@ __global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t spl
   }
   const uint64_t m64 = __shfl_sync(0xffffffffu, best[1], 31);
   if (m64 != kEmptyKey) tau = fminf(tau, key_dist(m64));
+  if (thr0 != nullptr) tau = fminf(tau, thr0[qi]);  // every list excluded rows scoring >= thr0
   // exact distances of the (up to) 64 candidates: lane handles 2, full row each (rows are L2/HBM gathers)
   const float* q = Q + (size_t)qi * q_stride;
   float qn = 0.f;
@@ -460,11 +533,13 @@ __global__ void knn_rerank_kernel(const uint64_t* __restrict__ cand, int64_t spl
     const double xmax = (double)__uint_as_float(facts[0]);
     const double qnorm = sqrt((double)qn);
     const int D = dq * 4;
-    const bool exact = facts[1] != 0u && qint && qnorm * xmax < 8388608.0 && xmax * xmax < 16777216.0;
+    // integer data and queries: every product and partial sum of the MMA is an integer below 2^24 (partial dot
+    // products are bounded by ||q|| ||x|| (Cauchy-Schwarz), the norm pieces by ||x||^2) -> scores are exact
+    const bool exact = facts[1] != 0u && qint && xmax * xmax + 2.0 * qnorm * xmax < 16777216.0;
     double E = 0.0;
     if (!exact) {
       const double u = 1.0 / 512.0 + (D + 9) * 2.384185791015625e-07;  // 2^-9 + (D+9) 2^-22
-      E = (metric == 0 ? 2.0 : 1.0) * u * qnorm * xmax + (D + 1) * 5.9604644775390625e-08 * (xmax * xmax + qn) +
+      E = (metric == 0 ? 2.0 : 1.0) * u * qnorm * xmax + (D + 4) * 5.9604644775390625e-08 * (xmax * xmax + qn) +
           1e-30;
     }
     const double dk = (double)key_dist(kk) * (exact ? 1.0 : 1.0 + (D + 2) * 5.9604644775390625e-08);
@@ -522,8 +597,8 @@ struct TcPlan {
 TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
   TcPlan p;
   p.kc = (dq * 4 + TC_KC - 1) / TC_KC;
-  const size_t a_bytes = (size_t)p.kc * kAChunkBytes;
-  const size_t budget = 227 * 1024 - 1024 - 512 - kTcEpiWarps * 32 * 4;
+  const size_t a_bytes = (size_t)(p.kc + 1) * kAChunkBytes;  // + the norm-weight chunk
+  const size_t budget = 227 * 1024 - 1024 - 512;
   p.stages = (int)std::min<size_t>(6, (budget - a_bytes) / kBStageBytes);
   p.qtiles = (nq + TC_M - 1) / TC_M;
   const int64_t ntiles = std::max<int64_t>(1, (n + TC_N - 1) / TC_N);
@@ -533,7 +608,7 @@ TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
   p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
   if (p.splits < 1) p.splits = 1;
   p.units = p.qtiles * p.splits;
-  p.smem = 1024 + a_bytes + (size_t)p.stages * kBStageBytes + 512 + kTcEpiWarps * 32 * 4;
+  p.smem = 1024 + a_bytes + (size_t)p.stages * kBStageBytes + 512;
   return p;
 }
 
@@ -541,23 +616,34 @@ TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
 
 bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k) {
   const int kc = (dq * 4 + TC_KC - 1) / TC_KC;
-  return k <= 32 && (q_stride * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0 &&
-         (size_t)kc * kAChunkBytes + 2 * kBStageBytes + 2048 <= 227 * 1024 && get_encode() != nullptr;
+  (void)q_stride;
+  (void)Q;  // queries are restaged into the A layout
+  return k <= 32 && (size_t)(kc + 1) * kAChunkBytes + 2 * kBStageBytes + 2048 <= 227 * 1024 && get_encode() != nullptr;
+}
+
+// the sample pass: enough rows that few rows of the full set beat its k-th (~ k n / S per query), few enough that
+// it costs a few percent of the main pass
+static int64_t sample_rows(int64_t n, int64_t nq) {
+  if (n < 262144 || nq < 512) return 0;
+  return std::min<int64_t>(65536, std::max<int64_t>(16384, n / 16)) / TC_N * TC_N;
 }
 
 size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
+  const int64_t S = sample_rows(n, nq);
+  const size_t sample = S ? knn_tc_scratch_bytes(nq, S, dq, k) + (size_t)nq * (k * 8 + 4) + 768 : 0;
   TcPlan p = tc_plan(nq, n, dq, 148);
   TcPlan p2 = tc_plan(nq, n, dq, 512);
   const int64_t s = std::max(p.splits, p2.splits);
-  // cand + norms + facts + fail list + fallback buffers (rows, ids, dists) + FFMA fallback scratch
-  return (size_t)s * 2 * nq * TC_LIST_MAX * 8 + (size_t)n * 4 + 1024 + (size_t)nq * 4 + (size_t)nq * dq * 16 +
-         (size_t)nq * k * 8 + knn_scratch_bytes(nq, k, n) + 8 * 256;
+  // cand + norm pieces + staged queries + facts + fail list + fallback buffers (rows, ids, dists) + FFMA scratch
+  return (size_t)s * 2 * nq * TC_LIST_MAX * 8 + (size_t)n * 128 + (size_t)nq * (p.kc + 1) * 128 + 1024 +
+         (size_t)nq * 4 + (size_t)nq * dq * 16 + (size_t)nq * k * 8 + knn_scratch_bytes(nq, k, n) + 10 * 256 +
+         sample;
 }
 
-cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
+static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
                           int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
                           uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
-                          cudaStream_t st, uint32_t* n_fallback) {
+                          cudaStream_t st, uint32_t* n_fallback, bool inner) {
   if (nq <= 0) return cudaSuccess;
   TcPlan p = tc_plan(nq, n, dq, num_sms);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -565,8 +651,10 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   uint64_t* cand = reinterpret_cast<uint64_t*>(sp);
   const int KL = k <= 16 ? 16 : 32;
   sp += al((size_t)p.splits * 2 * nq * KL * 8);
-  float* norms = reinterpret_cast<float*>(sp);
-  sp += al((size_t)n * 4);
+  float* npieces = reinterpret_cast<float*>(sp);  // [n][32]: ||x||^2 pieces (B's extra K chunk)
+  sp += al((size_t)n * 128);
+  float* qa = reinterpret_cast<float*>(sp);       // [nq][(kc+1)*32]: the staged A rows
+  sp += al((size_t)nq * (p.kc + 1) * 128);
   unsigned int* facts = reinterpret_cast<unsigned int*>(sp);  // [0] max norm bits, [1] integral, [2] n_fail
   sp += 256;
   uint32_t* fail_list = reinterpret_cast<uint32_t*>(sp);
@@ -577,23 +665,52 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   sp += al((size_t)nq * k * 4);
   float* fb_d = reinterpret_cast<float*>(sp);
   sp += al((size_t)nq * k * 4);
+  float* thr0 = nullptr;
+  const int64_t S = (self_base < 0 && !inner) ? sample_rows(n, nq) : 0;
+  uint32_t* s_ids = nullptr;
+  float* s_d = nullptr;
+  if (S > 0) {
+    thr0 = reinterpret_cast<float*>(sp);
+    sp += al((size_t)nq * 4);
+    s_ids = reinterpret_cast<uint32_t*>(sp);
+    sp += al((size_t)nq * k * 4);
+    s_d = reinterpret_cast<float*>(sp);
+    sp += al((size_t)nq * k * 4);
+  }
   if ((size_t)(sp - static_cast<unsigned char*>(scratch)) > scratch_bytes) return cudaErrorInvalidValue;
   const size_t rest = scratch_bytes - (size_t)(sp - static_cast<unsigned char*>(scratch));
+  if (S > 0) {
+    // exact k-NN over the first S rows (same engine, no further sampling): its k-th distance bounds the true one
+    // k distinct live rows with their exact distances bound the true k-th from above whether or not the
+    // sample's own certificate holds, so the sample pass needs neither the fallback nor a host synchronisation
+    cudaError_t es = knn_tc_impl(vec, dq, S, tomb, Q, q_stride, q_dim, nq, k, metric, -1, s_ids, s_d, sp, rest,
+                                 num_sms, st, nullptr, true);
+    if (es != cudaSuccess) return es;
+  }
 
-  CUtensorMap qmap, xmap;
-  if (!make_map(&qmap, Q, (uint64_t)q_dim, (uint64_t)nq, (uint64_t)q_stride * 4, TC_M) ||
-      !make_map(&xmap, vec, (uint64_t)dq * 4, (uint64_t)n, (uint64_t)dq * 16, TC_N))
+  const uint64_t qa_w = (uint64_t)(p.kc + 1) * 32;
+  CUtensorMap qmap, xmap, nmap;
+  if (!make_map(&qmap, qa, qa_w, (uint64_t)nq, qa_w * 4, TC_M) ||
+      !make_map(&xmap, vec, (uint64_t)dq * 4, (uint64_t)n, (uint64_t)dq * 16, TC_N) ||
+      !make_map(&nmap, npieces, 32, (uint64_t)n, 128, TC_N))
     return cudaErrorInvalidValue;
   unsigned int init[3] = {0u, 1u, 0u};
   cudaError_t e = cudaMemcpyAsync(facts, init, sizeof init, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
-  row_norms_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(vec, dq * 4, n, norms, facts);
-  TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, norms, tomb, self_base, metric, cand};
+  row_norms_kernel<<<(unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms * 8), 256, 0, st>>>(vec, dq * 4, n,
+                                                                                                   npieces, facts);
+  stage_queries_kernel<<<(unsigned)((nq * (int64_t)qa_w + 255) / 256), 256, 0, st>>>(Q, q_stride, q_dim, nq, p.kc,
+                                                                                       metric, qa);
+  if (S > 0)
+    prune_threshold_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(Q, q_stride, q_dim, nq, k, s_d, metric,
+                                                                         dq * 4, facts, thr0);
+  TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, nullptr, tomb, self_base, metric, cand,
+           metric == 0 ? 1 : 0, thr0};
   auto launch = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     if (e2 != cudaSuccess) return e2;
     const unsigned grid = (unsigned)std::min<int64_t>(p.units, num_sms);
-    kern<<<grid, kTcThreads, p.smem, st>>>(qmap, xmap, a);
+    kern<<<grid, kTcThreads, p.smem, st>>>(qmap, xmap, nmap, a);
     return cudaGetLastError();
   };
   if (KL == 16) {
@@ -611,12 +728,13 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
   if (KL == 16)
     knn_rerank_kernel<16><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride,
                                                                     q_dim, metric, facts, out_ids, out_d, fail_list,
-                                                                    facts + 2);
+                                                                    facts + 2, thr0);
   else
     knn_rerank_kernel<32><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(cand, p.splits * 2, nq, k, vec, dq, Q, q_stride,
                                                                     q_dim, metric, facts, out_ids, out_d, fail_list,
-                                                                    facts + 2);
+                                                                    facts + 2, thr0);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (inner) return cudaSuccess;
   // exact FFMA fallback for the queries the certificate rejected
   unsigned int hf = 0;
   if ((e = cudaMemcpyAsync(&hf, facts + 2, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
@@ -635,6 +753,14 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
+                          int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
+                          uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
+                          cudaStream_t st, uint32_t* n_fallback) {
+  return knn_tc_impl(vec, dq, n, tomb, Q, q_stride, q_dim, nq, k, metric, self_base, out_ids, out_d, scratch,
+                     scratch_bytes, num_sms, st, n_fallback, false);
 }
 
 }  // namespace svf
