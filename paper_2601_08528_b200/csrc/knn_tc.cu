@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -624,8 +625,12 @@ bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k) {
 // the sample pass: enough rows that few rows of the full set beat its k-th (~ k n / S per query), few enough that
 // it costs a few percent of the main pass
 static int64_t sample_rows(int64_t n, int64_t nq) {
-  if (n < 262144 || nq < 512) return 0;
-  return std::min<int64_t>(65536, std::max<int64_t>(16384, n / 16)) / TC_N * TC_N;
+  static const int64_t div = [] {  // SVF_KNN_SAMPLE_DIV: tuning override of the sample fraction 1/div (0 = off)
+    const char* v = getenv("SVF_KNN_SAMPLE_DIV");
+    return v ? (int64_t)atoll(v) : (int64_t)16;
+  }();
+  if (div <= 0 || n < 262144 || nq < 512) return 0;
+  return std::min<int64_t>(65536, std::max<int64_t>(8192, n / div)) / TC_N * TC_N;
 }
 
 size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
