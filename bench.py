@@ -294,7 +294,7 @@ def run_svf(a):
             t1 = time.perf_counter()
             idx.search_into(Qh, k, L, oi_h, od_h)          # H2D + kernel + D2H + sync inside svf_search
             tt.append(time.perf_counter() - t1)
-        e2e_s = D.max(float(np.mean(tt)))
+        e2e_s = D.max(float(np.median(tt)))              # host wall time per step: median (robust to host jitter)
         e2e = {"value": round(nq * D.world / e2e_s, 1), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 8)}
 

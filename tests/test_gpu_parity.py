@@ -324,35 +324,61 @@ def test_search_large_batch_all_modes_bit_exact(svf, c1, wpq):
     assert idx.last_search_counters()["iters"] == rc[:, 2].sum()
 
 
+@pytest.fixture(scope="module")
+def c1r64():
+    """C1 data with a degree-64 graph (the handoff needs degree * search_width > 32: two candidate registers)."""
+    X = base_rows("C1")
+    g, e = oracle.build(X, R=64)
+    return X, g, e
+
+
 @pytest.mark.parametrize("L,pct", [(32, 100), (32, 30), (14, 50), (128, 100), (64, 0)])
-def test_search_handoff_bit_exact(svf, c1, L, pct):
+def test_search_handoff_bit_exact(svf, c1r64, L, pct):
     """Pair-mode handoff of the batch's stragglers (svf_set_search_handoff): queries suspended by the one-warp grid
     and resumed by the chained pair-mode grid (pool + counters carried over, visited table rebuilt from the pool,
     reading I7) give the oracle's ids, distances, iterations and expansions bit for bit.  pct = 100 suspends every
-    query still running once the first warp has left."""
-    X, Q, g, e = c1
+    query still running once the first warp has left; the launch count proves the resume grid ran."""
+    X, g, e = c1r64
     from workloads import query_rows as qr
 
     Qb = qr("C1", 6000)
     idx = svf.Index.from_state(X, g, e)
     idx.set_warps_per_query(1)
     idx.set_search_handoff(pct)
+    dead = np.arange(0, len(X), 11, dtype=np.uint32)       # with tombstones
+    idx.delete(cuda(dead.astype(np.int32)))
+    tomb = pack_tomb(dead, len(X))
+    ri, rd, rc = oracle.graph_search(X, g, Qb, 10, L, tomb=tomb)
     for rep in range(2):                                # slots are freed for reuse by the next launch
         idx.set_trace(rep == 1)                         # the diagnostic timeline rides along (no effect)
         ids, d = idx.search(cuda(Qb), 10, L)
-        ri, rd, rc = oracle.graph_search(X, g, Qb, 10, L)
         assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
         cnt = idx.last_search_counters()
+        assert cnt["launches"] == (2 if pct > 0 else 1)
         assert cnt["iters"] == rc[:, 2].sum() and cnt["n_exp"] == rc[:, 1].sum()
         assert cnt["n_dist"] >= rc[:, 0].sum()
     t0, t1, _, it, _ = idx.read_trace(len(Qb))
     assert len(t0) == len(Qb) and (t1 >= t0).all() and np.array_equal(it, rc[:, 2])
 
 
-def test_search_handoff_mixed_pool_sizes(svf, c1):
+def test_search_handoff_ip_metric(svf):
+    """The handoff on an inner-product index (D=200, degree 64), integer data: bit-exact against the oracle."""
+    gen = GLM(dim=200, ell=16, integer=True)
+    X, Q = gen.rows(3, 3, 0, 6000), gen.rows(3, 4, 0, 5000)
+    g, e = oracle.build(X, R=64, metric=1)
+    idx = svf.Index.from_state(X, g, e, metric=1)
+    idx.set_warps_per_query(1)
+    idx.set_search_handoff(100)
+    ids, d = idx.search(cuda(Q), 10, 48)
+    ri, rd, _ = oracle.graph_search(X, g, Q, 10, 48, metric=1)
+    assert idx.last_search_counters()["launches"] == 2
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+def test_search_handoff_mixed_pool_sizes(svf, c1r64):
     """Handoff slots are shared by every pool size of an index: alternating itopk (different register layouts of
     the suspended pools) must never leave a stale slot that a later launch mistakes for a published one."""
-    X, Q, g, e = c1
+    X, g, e = c1r64
     from workloads import query_rows as qr
 
     Qb = qr("C1", 6000)
@@ -362,6 +388,7 @@ def test_search_handoff_mixed_pool_sizes(svf, c1):
     for L in (128, 32, 96, 16, 128, 14):
         ids, d = idx.search(cuda(Qb), 10, L)
         ri, rd, _ = oracle.graph_search(X, g, Qb, 10, L)
+        assert idx.last_search_counters()["launches"] == 2
         assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd), L
 
 

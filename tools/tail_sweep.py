@@ -23,10 +23,12 @@ def main():
     ap.add_argument("--reps", type=int, default=60)
     ap.add_argument("--batches", default="10000")
     ap.add_argument("--tails", default="0,10,20,30,40,60", help="handoff thresholds (%% of warps)")
+    ap.add_argument("--hash-bits", type=int, default=0, help="visited-table slots 2^b (0 = auto)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     idx = svf.Index.build(torch.from_numpy(base_rows("C2")).to(dev), degree=64)
+    idx.set_search_params(1, 0, 0, a.hash_bits)
     nqmax = max(int(b) for b in a.batches.split(","))
     Qall = torch.from_numpy(query_rows("C2", nqmax)).to(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
