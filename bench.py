@@ -69,13 +69,17 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if self.world != n_gpus and self.world > 1:
             raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.world}")
-        self.dev = torch.device("cuda", self.local)
+        # SVF_SAME_DEVICE=1 + SVF_BACKEND=gloo: every rank on cuda:0 (checks the N>1 plumbing on a 1-GPU box;
+        # NCCL refuses two ranks on one device).  Production runs use one GPU per rank over NCCL.
+        same = os.environ.get("SVF_SAME_DEVICE") == "1"
+        self.dev = torch.device("cuda", 0 if same else self.local)
         torch.cuda.set_device(self.dev)
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.init_process_group("nccl", device_id=self.dev)
+            backend = os.environ.get("SVF_BACKEND", "nccl")
+            dist.init_process_group(backend, device_id=self.dev if backend == "nccl" else None)
             self.pg = dist
 
     def barrier(self):
@@ -175,7 +179,7 @@ def run_svf(a):
     torch.cuda.synchronize()
     t0 = time.time()
     idx = svf.Index.build(Xd, degree=R, metric=c["metric"], capacity=n + (0 if Xnew is None else len(Xnew)),
-                          device=D.local, search_width=a.search_width)
+                          device=D.dev.index, search_width=a.search_width)
     torch.cuda.synchronize()
     t_build = time.time() - t0
     del Xd
