@@ -288,11 +288,11 @@ def run_svf(a):
         Qh = torch.from_numpy(Q).pin_memory()
         oi_h = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)   # pinned result buffers, reused
         od_h = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
-        for _ in range(max(3, a.warmup // 4)):
+        for _ in range(max(10, a.warmup // 2)):
             idx.search_into(Qh, k, L, oi_h, od_h)
         D.barrier()
         tt = []
-        for _ in range(max(10, a.steps // 4)):
+        for _ in range(max(30, a.steps // 2)):
             flush.zero_()
             torch.cuda.synchronize()
             t1 = time.perf_counter()
@@ -300,7 +300,8 @@ def run_svf(a):
             tt.append(time.perf_counter() - t1)
         e2e_s = D.max(float(np.median(tt)))              # host wall time per step: median (robust to host jitter)
         e2e = {"value": round(nq * D.world / e2e_s, 1), "unit": "queries/s",
-               "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 8)}
+               "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 8),
+               "host_ms_p10_p50_p90": [round(float(np.percentile(tt, p)) * 1e3, 4) for p in (10, 50, 90)]}
 
     # ---- CPU baseline: the oracle, as it stands, on the host cores, on the graph just timed (rank 0, N=1 only) ------
     cpu, alg = None, None
@@ -339,6 +340,13 @@ def run_svf(a):
             e1.record()
             torch.cuda.synchronize()
             t_del.append(e0.elapsed_time(e1))
+        # algorithmic bytes per insert: B_i = B_q(L_insert) + |C| R 4 + 2 R (R 8) + (D 4 + R 8), with the
+        # L_insert = 128 search's counters measured by an itopk-128 search over the same index (GPU counters)
+        Lins = 128
+        sh.local.search(Qd, Lins, Lins)
+        ic = idx.last_search_counters()
+        nd_i, ne_i = ic["n_dist"] / max(1, ic["queries"]), ic["n_exp"] / max(1, ic["queries"])
+        b_i = (nd_i * dim * 4 + ne_i * R * 4 + dim * 4 + Lins * 8) + Lins * R * 4 + 2 * R * (R * 8) + (dim * 4 + R * 8)
         ins_ms, del_ms = D.max(float(np.mean(t_ins))), D.max(float(np.mean(t_del)))
         ins = {"inserts_per_s": round(ins_batch * D.world / (ins_ms / 1e3), 1),
                "deletes_per_s": round(ins_batch * D.world / (del_ms / 1e3), 1),
@@ -346,6 +354,12 @@ def run_svf(a):
                "insert_breakdown_ms": {kk: round(v[0] / max(1, ins_warm + ins_steps), 3)
                                        for kk, v in iprof.items() if kk != "search"},
                "build_inserts_per_s": round(n / t_build, 1)}
+        pk = measured_peaks().get("hbm_gbs", 6650.0)
+        ach = ins_batch / (ins_ms / 1e3) * b_i / 1e9
+        ins["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s",
+                           "frac": round(ach / pk, 4), "alg_bytes_per_insert": round(b_i, 1),
+                           "alg_counts": {"n_dist": round(nd_i, 2), "n_exp": round(ne_i, 2),
+                                          "source": "GPU counters of an itopk-128 search over the same index"}}
 
     if alg is None:
         alg = {"n_dist": gpu_counters["n_dist"] / max(1, gpu_counters["queries"]),
