@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 from workloads import base_rows, config_spec, query_rows  # noqa: E402
 
-L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 48, 64, 96, 128, 192, 256]
+L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 48, 64, 80, 96, 128, 192, 256]
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}

@@ -162,7 +162,9 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   while ((1 << minbits) < idx->Dp) ++minbits;                  // the table also stages the query row
   // default: small tables buy occupancy (the search is latency-bound); forgetting costs ~10% extra distances
   // at small L (measured: C2 L=14, 1024 slots 9.9M QPS vs 2048 slots 9.5M vs 4096 slots 7.3M)
-  const int autobits = L <= 16 ? 10 : (L <= 48 ? 11 : (L <= 128 ? 12 : 13));
+  // 2048 slots up to L = 128 (C3 10M x 96 at L = 96: 4.96 vs 5.40 ms with 4096 slots, C2 inserts at L = 128
+  // 7.1 vs 7.2 ms; tools/param_sweep.py, tools/insert_rate.py)
+  const int autobits = L <= 16 ? 10 : (L <= 128 ? 11 : 13);
   c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   if (c.hbits > 15) return why = "hash_bits too large", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);

@@ -21,6 +21,8 @@ t0 = time.time()
 idx = svf.Index.build(X, degree=64, capacity=1_120_000)
 torch.cuda.synchronize()
 t_build = time.time() - t0
+hb = int(os.environ.get("SVF_HB", "0"))  # visited-table bits for the timed inserts (0 = automatic)
+idx.set_search_params(1, 0, 0, hb)
 idx.insert(Xn[:20_000])
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,6 +32,6 @@ for i in range(10):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-print(json.dumps({"handoff_env": os.environ.get("SVF_HANDOFF"), "build_s": round(t_build, 3),
+print(json.dumps({"handoff_env": os.environ.get("SVF_HANDOFF"), "hash_bits": hb, "build_s": round(t_build, 3),
                   "build_inserts_per_s": round(1e6 / t_build), "insert_ms_per_10k": round(ms, 3),
                   "inserts_per_s": round(1e4 / (ms / 1e3))}))
