@@ -18,8 +18,11 @@ constexpr size_t handoff_words() { return 8 + (size_t)kHandoffMaxWarps * (4 + 32
 #ifndef SVF_MINB_PAIR
 #define SVF_MINB_PAIR 4
 #endif
+#ifndef SVF_MINB4
+#define SVF_MINB4 4
+#endif
 constexpr int search_min_blocks(int kpl, int wpq = 1) {
-  return wpq == 2 ? SVF_MINB_PAIR : kpl <= 1 ? SVF_MINB1 : kpl <= 2 ? 5 : kpl <= 4 ? 4 : kpl <= 8 ? 3 : 2;
+  return wpq == 2 ? SVF_MINB_PAIR : kpl <= 1 ? SVF_MINB1 : kpl <= 2 ? 5 : kpl <= 4 ? SVF_MINB4 : kpl <= 8 ? 3 : 2;
 }
 // vectors per distance team per gather round: the throughput (one-warp) kernel keeps 2 (more costs occupancy);
 // the latency kernels (pair mode: small batches and the batch tail) gather deeper per round
@@ -29,7 +32,7 @@ constexpr int search_min_blocks(int kpl, int wpq = 1) {
 #ifndef SVF_GATHER_U_PAIR
 #define SVF_GATHER_U_PAIR 4
 #endif
-constexpr int gather_u(int wpq) { return wpq == 2 ? SVF_GATHER_U_PAIR : SVF_GATHER_U; }
+
 
 struct SearchArgs {
   const float* vec;        // [cap][dq*4]

@@ -81,6 +81,16 @@ struct Geo {
   static constexpr int NV = (DQT + T - 1) / T;
 };
 
+// Gather depth (vectors per team per round): the one-warp kernel keeps 2 at small pools (more costs occupancy);
+// pools of >= 128 keys run at 4 blocks/SM whatever the depth (their register limit is 128 either way), so they
+// go as deep as fits without spills: 4 when a lane holds <= 3 float4 of a row (D = 96), else 3 (D = 128, 200);
+// the pair-mode (latency) kernels use SVF_GATHER_U_PAIR at 32-key pools, 2 above.
+template <int WPQ, int KPL, int DQT>
+constexpr int gather_u() {
+  return WPQ == 2 ? (KPL == 1 ? SVF_GATHER_U_PAIR : 2)  // deeper pair rounds spill once the pool is >= 64 keys
+                  : (KPL >= 4 && DQT > 0) ? (Geo<DQT>::NV <= 3 ? 4 : 3) : SVF_GATHER_U;
+}
+
 // Distances of this warp's S survivors sid[0..S) -> keys; keep those strictly better than the pool's current L-th
 // key (the only ones that can enter: the pool keeps the L smallest of pool U cand), compacted into skey[0..S2).
 template <int KPL, int CPL, int DQT, int U>
@@ -394,7 +404,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         }
         const int kept = min(running, a.n_init - taken);
         taken += kept;
-        const int S2 = score_own<KPL, CPL, DQT, gather_u(WPQ)>(a, pool, sid, keys_of(h, par), mine, qv, lane);
+        const int S2 = score_own<KPL, CPL, DQT, gather_u<WPQ, KPL, DQT>()>(a, pool, sid, keys_of(h, par), mine, qv, lane);
         exchange_merge(mine, S2);
       }
     }
@@ -517,7 +527,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
       SVF_PH(2)
       // S5: distances of this warp's survivors; S6: exchange + merge
       if (WPQ == 1 && running == 0) continue;
-      const int S2 = score_own<KPL, CPL, DQT, gather_u(WPQ)>(a, pool, sid, keys_of(h, par), running, qv, lane);
+      const int S2 = score_own<KPL, CPL, DQT, gather_u<WPQ, KPL, DQT>()>(a, pool, sid, keys_of(h, par), running, qv, lane);
       SVF_PH(3)
       exchange_merge(running, S2);
       SVF_PH(4)
