@@ -131,7 +131,6 @@ struct TcArgs {
   int stages;            // B ring depth
   int64_t rows_per_split;
   int64_t splits, units; // units = qtiles * splits
-  const float* unused_norms;
   const uint32_t* tomb;
   int64_t self_base;     // >= 0: exclude id == self_base + query
   int metric;
@@ -709,7 +708,7 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
   if (S > 0)
     prune_threshold_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(Q, q_stride, q_dim, nq, k, s_d, metric,
                                                                          dq * 4, facts, thr0);
-  TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, nullptr, tomb, self_base, metric, cand,
+  TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, tomb, self_base, metric, cand,
            metric == 0 ? 1 : 0, thr0};
   auto launch = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
