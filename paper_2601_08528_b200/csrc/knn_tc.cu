@@ -594,7 +594,7 @@ struct TcPlan {
   int64_t splits, rows_per_split, units, qtiles;
   size_t smem;
 };
-TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
+TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms, int units_per_sm = 8) {
   TcPlan p;
   p.kc = (dq * 4 + TC_KC - 1) / TC_KC;
   const size_t a_bytes = (size_t)(p.kc + 1) * kAChunkBytes;  // + the norm-weight chunk
@@ -602,7 +602,7 @@ TcPlan tc_plan(int64_t nq, int64_t n, int dq, int num_sms) {
   p.stages = (int)std::min<size_t>(6, (budget - a_bytes) / kBStageBytes);
   p.qtiles = (nq + TC_M - 1) / TC_M;
   const int64_t ntiles = std::max<int64_t>(1, (n + TC_N - 1) / TC_N);
-  int64_t s = std::max<int64_t>(1, (8LL * num_sms + p.qtiles - 1) / p.qtiles);  // ~8 units per SM
+  int64_t s = std::max<int64_t>(1, ((int64_t)units_per_sm * num_sms + p.qtiles - 1) / p.qtiles);  // ~8 units/SM
   s = std::min(s, ntiles);
   p.rows_per_split = (ntiles + s - 1) / s * TC_N;
   p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
@@ -626,7 +626,7 @@ bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k) {
 static int64_t sample_rows(int64_t n, int64_t nq) {
   static const int64_t div = [] {  // SVF_KNN_SAMPLE_DIV: tuning override of the sample fraction 1/div (0 = off)
     const char* v = getenv("SVF_KNN_SAMPLE_DIV");
-    return v ? (int64_t)atoll(v) : (int64_t)16;
+    return v ? (int64_t)atoll(v) : (int64_t)32;  // n/32 rows (C2: 5.75 ms vs 5.83 at n/16, 7.2 without)
   }();
   if (div <= 0 || n < 262144 || nq < 512) return 0;
   return std::min<int64_t>(65536, std::max<int64_t>(8192, n / div)) / TC_N * TC_N;
@@ -649,7 +649,12 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
                           uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
                           cudaStream_t st, uint32_t* n_fallback, bool inner) {
   if (nq <= 0) return cudaSuccess;
-  TcPlan p = tc_plan(nq, n, dq, num_sms);
+  // the sample pass: ~4 units per SM (C2: 5.75 vs 5.92 ms end to end at 8; 2 and 16 were no better)
+  static const int inner_ups = [] {  // SVF_KNN_INNER_UPS: tuning override
+    const char* v = getenv("SVF_KNN_INNER_UPS");
+    return v ? atoi(v) : 4;
+  }();
+  TcPlan p = tc_plan(nq, n, dq, num_sms, inner ? inner_ups : 8);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   unsigned char* sp = static_cast<unsigned char*>(scratch);
   uint64_t* cand = reinterpret_cast<uint64_t*>(sp);
