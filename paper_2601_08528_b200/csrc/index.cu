@@ -35,6 +35,12 @@ struct svf_index {
   int64_t trace_cap = 0, trace_nq = 0;
   int64_t counters_cap = 0, counters_nq = 0;
   cudaStream_t last_stream = nullptr;
+  // streamed host queries (svf_search with a host Q): copy stream, chunk flags, pinned epoch ring
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_cs0 = nullptr, ev_cs1 = nullptr;
+  unsigned int* q_flags = nullptr;
+  unsigned int* h_epoch = nullptr;  // pinned ring of epoch values (copy sources)
+  unsigned int epoch = 0;
   bool poisoned = false;
   int search_width = 1, n_init = 0, max_iter = 0, hash_bits = 0;
   int knn_mode = 0;                     // 0 auto (tcgen05 when supported), 1 FFMA only
@@ -209,6 +215,51 @@ void prof_resolve(svf_index* idx) {
   idx->prof_pending.clear();
 }
 
+// Host queries are copied in chunks on the index's copy stream, each chunk followed by a 4-byte flag copy (copy
+// engine only: no SM is needed to publish it, so a search grid spinning on the flags cannot starve it); the search
+// starts at once and each query waits for its chunk.  Epochs make stale flags of earlier calls harmless.
+struct StreamedQ {
+  bool active;
+  unsigned int* flags;
+  unsigned int epoch;
+  int chunk_log2;
+};
+constexpr int kMaxQChunks = 4096;
+cudaError_t stream_queries(svf_index* idx, const float* Q, int64_t nq, char* dst, cudaStream_t st, StreamedQ& sq) {
+  cudaError_t e;
+  if (idx->cstream == nullptr) {
+    if ((e = cudaStreamCreateWithFlags(&idx->cstream, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&idx->ev_cs0, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&idx->ev_cs1, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&idx->q_flags, kMaxQChunks * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemset(idx->q_flags, 0, kMaxQChunks * 4)) != cudaSuccess) return e;
+    if ((e = cudaHostAlloc(&idx->h_epoch, 64 * 4, cudaHostAllocDefault)) != cudaSuccess) return e;
+  }
+  int lg = 9;  // 512 queries per chunk (256 KB at D = 128)
+  while ((nq + (1LL << lg) - 1) >> lg > kMaxQChunks) ++lg;
+  const int64_t nchunks = (nq + (1LL << lg) - 1) >> lg;
+  // the previous call's chunk copies have run (normally long ago), so no pending copy still reads a ring slot
+  if ((e = cudaEventSynchronize(idx->ev_cs1)) != cudaSuccess) return e;
+  idx->epoch = idx->epoch + 1 == 0 ? 1 : idx->epoch + 1;
+  unsigned int* src = idx->h_epoch + (idx->epoch & 63);
+  *src = idx->epoch;
+  // the copy stream starts after everything already queued on st (the staging buffer may still be in use)
+  if ((e = cudaEventRecord(idx->ev_cs0, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(idx->cstream, idx->ev_cs0, 0)) != cudaSuccess) return e;
+  const size_t row = (size_t)idx->D * 4;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r0 = c << lg, r1 = std::min<int64_t>(nq, (c + 1) << lg);
+    if ((e = cudaMemcpyAsync(dst + r0 * row, Q + r0 * idx->D, (size_t)(r1 - r0) * row, cudaMemcpyHostToDevice,
+                             idx->cstream)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemcpyAsync(idx->q_flags + c, src, 4, cudaMemcpyHostToDevice, idx->cstream)) != cudaSuccess) return e;
+  }
+  // later work on st (the next call's staging) waits for the copies
+  if ((e = cudaEventRecord(idx->ev_cs1, idx->cstream)) != cudaSuccess) return e;
+  sq = {true, idx->q_flags, idx->epoch, lg};
+  return cudaSuccess;
+}
+
 // default handoff threshold: 45% of the one-warp grid's warps (C2, itopk 14, tools/tail_sweep.py: 10K batch
 // 0.836 -> 0.758 ms, 20K 1.359 -> 1.313 ms, 40K 2.553 -> 2.479 ms; 25/35/55% were no better at any batch);
 // SVF_HANDOFF overrides it for tuning
@@ -224,7 +275,7 @@ int handoff_auto() {
 cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_dim, int64_t nq, uint64_t n_snapshot,
                        uint64_t qidx_base, int L, int n_out, const SearchCfg& c, int p, int max_iter,
                        uint32_t* out_ids, float* out_d, uint32_t* counters, int prof_slot, cudaStream_t st,
-                       bool update_path) {
+                       bool update_path, const StreamedQ* sq = nullptr) {
   SearchArgs a{};
   a.vec = idx->vec;
   a.dq = idx->dq;
@@ -252,6 +303,9 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.out_d = out_d;
   a.counters = counters;
   a.trace = idx->trace_on && counters != nullptr && idx->trace_cap >= nq ? idx->trace : nullptr;
+  a.q_flags = sq ? sq->flags : nullptr;
+  a.q_epoch = sq ? sq->epoch : 0u;
+  a.q_chunk_log2 = sq ? sq->chunk_log2 : 0;
   // the two paths own disjoint queue counters and handoff buffers, so an svf_search on one stream may overlap an
   // update on another; svf_search snapshots n at each query's start from n_visible
   a.work_counter = idx->small + (update_path ? 5 : 4);
@@ -553,8 +607,9 @@ svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int
   CK(idx, ensure_sscratch(idx, qb + 2 * ob, st), "search scratch");
   char* sp = static_cast<char*>(idx->sscratch);
   const float* Qd = Q;
+  StreamedQ sq{};
   if (!q_dev) {
-    CK(idx, cudaMemcpyAsync(sp, Q, (size_t)nq * idx->D * 4, cudaMemcpyHostToDevice, st), "H2D queries");
+    CK(idx, stream_queries(idx, Q, nq, sp, st, sq), "H2D queries");
     Qd = reinterpret_cast<const float*>(sp);
   }
   uint32_t* oi = i_dev ? out_ids : reinterpret_cast<uint32_t*>(sp + qb);
@@ -578,8 +633,9 @@ svf_status svf_search(svf_index* idx, const float* Q, int64_t nq, int32_t k, int
   idx->last_stream = st;
   CK(idx,
      run_search(idx, Qd, idx->D, idx->D, nq, (uint64_t)idx->n_alloc, 0, itopk, k, c, idx->search_width,
-                idx->max_iter, oi, od, idx->counters, 0, st, false),
+                idx->max_iter, oi, od, idx->counters, 0, st, false, sq.active ? &sq : nullptr),
      "search kernel");
+  if (sq.active) CK(idx, cudaStreamWaitEvent(st, idx->ev_cs1, 0), "join copy stream");
   if (!i_dev) CK(idx, cudaMemcpyAsync(out_ids, oi, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H ids");
   if (!d_dev) CK(idx, cudaMemcpyAsync(out_dists, od, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st), "D2H dists");
   if (!i_dev || !d_dev) CK(idx, cudaStreamSynchronize(st), "search sync");
@@ -972,6 +1028,11 @@ svf_status svf_destroy(svf_index* idx) {
   if (idx->trace) cudaFree(idx->trace);
   if (idx->ho) cudaFree(idx->ho);
   if (idx->ho_upd) cudaFree(idx->ho_upd);
+  if (idx->q_flags) cudaFree(idx->q_flags);
+  if (idx->h_epoch) cudaFreeHost(idx->h_epoch);
+  if (idx->ev_cs0) cudaEventDestroy(idx->ev_cs0);
+  if (idx->ev_cs1) cudaEventDestroy(idx->ev_cs1);
+  if (idx->cstream) cudaStreamDestroy(idx->cstream);
   if (idx->ev0) cudaEventDestroy(idx->ev0);
   if (idx->ev1) cudaEventDestroy(idx->ev1);
   for (auto& r : idx->prof_pending) {

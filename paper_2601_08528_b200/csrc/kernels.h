@@ -69,6 +69,11 @@ struct SearchArgs {
   // nullable: device word holding the ids whose insertion has completed; each query snapshots
   // n = min(n_alloc, *n_visible) at its start (svf_search overlapping an insert on another stream)
   const unsigned long long* n_visible;
+  // nullable: host queries streamed in chunks of 2^q_chunk_log2 rows on a copy stream; q_flags[c] == q_epoch once
+  // chunk c has landed (its flag is copied after it, in copy-stream order), so the search overlaps the H2D copy
+  const unsigned int* q_flags;
+  unsigned int q_epoch;
+  int q_chunk_log2;
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 

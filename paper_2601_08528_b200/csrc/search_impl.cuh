@@ -291,6 +291,12 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
   for (;;) {
     if (h == 0 && lane == 0) {
       const unsigned long long f = resume ? ho_take(a, ho_stride) : atomicAdd(counter, 1ull);
+      // streamed host queries: wait until this query's chunk has landed (a resumed query's chunk already has)
+      if (!resume && a.q_flags != nullptr && f < (unsigned long long)limit) {
+        const volatile unsigned int* fl = a.q_flags + ((base + f) >> a.q_chunk_log2);
+        while (*fl != a.q_epoch) __nanosleep(64);
+        __threadfence();
+      }
       qslot[0] = f;
       // the query's snapshot: ids below n exist (n_visible: inserts completed on another stream); resumed queries
       // keep the snapshot they started with
@@ -315,7 +321,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
     // the query is staged (coalesced) through the visited table, which is cleared right after (H >= Dp: host)
     const float* qg = a.Q + (size_t)qi * a.q_stride;
     float* qstage = reinterpret_cast<float*>(tab);
-    for (int i = h * 32 + lane; i < a.dq * 4; i += 32 * WPQ) qstage[i] = i < a.q_dim ? __ldg(qg + i) : 0.f;
+    for (int i = h * 32 + lane; i < a.dq * 4; i += 32 * WPQ) qstage[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
     qsync<WPQ>(slot);
     float4 qv[4];
 #pragma unroll
