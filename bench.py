@@ -27,6 +27,10 @@ sys.path.insert(0, ROOT)
 
 from workloads import base_rows, config_spec, query_rows  # noqa: E402
 
+# L_build per config (svf_params.build_itopk; reading I15): the graph is grown once at this candidate-list size, then
+# streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
+# recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
+BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
 L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 48, 64, 80, 96, 128, 192, 256]
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -47,6 +51,7 @@ def parse():
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--itopk", type=int, default=0, help="fix itopk (skip the sweep)")
     ap.add_argument("--search-width", type=int, default=1)
+    ap.add_argument("--build-itopk", type=int, default=-1, help="L_build (-1 = per-config default, 0 = insert_itopk)")
     ap.add_argument("--hash-bits", type=int, default=0, help="visited-table slots 2^b per query (0 = auto)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -177,9 +182,10 @@ def run_svf(a):
     Xd = torch.from_numpy(X).to(dev)
     Qd = torch.from_numpy(Q).to(dev)
     torch.cuda.synchronize()
+    build_L = a.build_itopk if a.build_itopk >= 0 else BUILD_ITOPK.get(a.config, 0)
     t0 = time.time()
     idx = svf.Index.build(Xd, degree=R, metric=c["metric"], capacity=n + (0 if Xnew is None else len(Xnew)),
-                          device=D.dev.index, search_width=a.search_width)
+                          device=D.dev.index, search_width=a.search_width, build_itopk=build_L)
     torch.cuda.synchronize()
     t_build = time.time() - t0
     del Xd
@@ -401,7 +407,7 @@ def run_svf(a):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-LM, integer-valued; DESIGN.md)",
             "config": {"workload": c["workload"], "n_per_gpu": n, "dim": dim, "degree": R, "batch": nq, "k": k,
-                       "itopk": L, "search_width": a.search_width, "recall_at_10": recall,
+                       "itopk": L, "search_width": a.search_width, "build_itopk": build_L, "insert_itopk": 128, "recall_at_10": recall,
                        "recall_sweep": sweep, "l2": "flushed between timed steps (256 MB write)",
                        "launch": "CUDA graph replay of svf_search" if graph is not None else "direct",
                        "parallelism": f"{D.world} shard(s), queries broadcast" +
@@ -460,8 +466,9 @@ def run_reference(a):
     Q = query_rows(a.config, nq)
     # Input preparation (untimed): the graph is built by svf_build, which is bit-identical to oracle.build on this
     # integer-valued workload (tests/test_gpu_parity.py::test_build_bit_exact_integer_data); exact ground truth by
-    # svf_knn_exact.  Only the oracle's search is timed.
-    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=R, metric=c["metric"])
+    # svf_knn_exact.  Only the oracle's search is timed.  Same L_build as the svf arm, so the same graph.
+    build_L = a.build_itopk if a.build_itopk >= 0 else BUILD_ITOPK.get(a.config, 0)
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=R, metric=c["metric"], build_itopk=build_L)
     gt, _ = idx.knn_exact(torch.from_numpy(Q).cuda(), k)
     gt = gt.cpu().numpy()
     st = idx.export()
@@ -497,7 +504,7 @@ def run_reference(a):
             "value": round(qps, 1), "unit": "queries/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64-accumulate (fp32 decisions)", "data": "synthetic (seeded G-LM, integer-valued)",
-            "config": {"workload": c["workload"], "n_per_gpu": n, "batch": nq, "k": k, "itopk": L,
+            "config": {"workload": c["workload"], "n_per_gpu": n, "batch": nq, "k": k, "itopk": L, "build_itopk": build_L,
                        "recall_sweep_1000q": sweep, "step_sample_queries": m},
             "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads, "kind": "oracle",
                              "sample": f"{m} queries per step at itopk={L}"},

@@ -71,6 +71,9 @@ typedef struct {
   int32_t hash_bits;      /* visited-table slots per query = 2^hash_bits (I7); 0 = automatic */
   uint64_t seed;          /* entry-point seed (I2, I18) */
   int32_t device;         /* CUDA ordinal the index lives on */
+  int32_t build_itopk;    /* L_build: candidate-list size of svf_build's growth inserts (I15); 0 = insert_itopk.
+                           * A larger L_build buys graph quality once, at build time; later svf_insert calls use
+                           * insert_itopk.  <= 512. */
 } svf_params;
 
 /* Fill *p with the defaults above for dimension `dim` and degree `degree` (metric L2, capacity 0). */

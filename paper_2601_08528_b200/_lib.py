@@ -25,7 +25,7 @@ class SvfParams(ctypes.Structure):
         ("capacity", ctypes.c_int64), ("search_width", ctypes.c_int32), ("n_init", ctypes.c_int32),
         ("max_iter", ctypes.c_int32), ("insert_itopk", ctypes.c_int32), ("protect_prefix", ctypes.c_int32),
         ("insert_batch", ctypes.c_int32), ("seed_size", ctypes.c_int32), ("hash_bits", ctypes.c_int32),
-        ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("device", ctypes.c_int32), ("build_itopk", ctypes.c_int32),
     ]
 
 

@@ -373,6 +373,7 @@ svf_status validate_params(const svf_params* p) {
   if (p->capacity < 1 || p->capacity > 0x7FFFFFFFll) return fail(SVF_ERR_INVALID, "capacity must be in [1, 2^31-1]");
   if (p->search_width < 1 || p->search_width > 8) return fail(SVF_ERR_INVALID, "search_width must be in [1, 8]");
   if (p->insert_itopk < 1 || p->insert_itopk > 512) return fail(SVF_ERR_INVALID, "insert_itopk must be in [1, 512]");
+  if (p->build_itopk < 0 || p->build_itopk > 512) return fail(SVF_ERR_INVALID, "build_itopk must be in [0, 512]");
   if (p->protect_prefix < -1 || p->protect_prefix > p->degree) return fail(SVF_ERR_INVALID, "bad protect_prefix");
   if (p->insert_batch < 1) return fail(SVF_ERR_INVALID, "insert_batch must be >= 1");
   if (p->seed_size < 1) return fail(SVF_ERR_INVALID, "seed_size must be >= 1");
@@ -421,8 +422,7 @@ svf_status alloc_index(const svf_params* p, svf_index** out) {
 }
 
 // insertion of rows [n_alloc, n_alloc + n) already present in vec (sub-batch snapshots, I13)
-svf_status insert_present_rows(svf_index* idx, int64_t n, cudaStream_t st) {
-  const int L = idx->p.insert_itopk;
+svf_status insert_present_rows(svf_index* idx, int64_t n, int L, cudaStream_t st) {
   SearchCfg c;
   std::string why;
   if (!search_cfg(idx, L, idx->p.search_width, idx->p.n_init, idx->hash_bits, c, why))
@@ -532,7 +532,7 @@ svf_status svf_build(const svf_params* p, const float* X, int64_t n, void* strea
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "seed exact R-NN"));
   idx->n_alloc = n0;
   if (n > n0) {
-    s = insert_present_rows(idx, n - n0, st);
+    s = insert_present_rows(idx, n - n0, idx->p.build_itopk ? idx->p.build_itopk : idx->p.insert_itopk, st);
     if (s != SVF_OK) return bail(s);
   }
   if ((e = launch_store_u64(idx->small + 6, (uint64_t)idx->n_alloc, st)) != cudaSuccess ||
@@ -655,7 +655,7 @@ svf_status svf_insert(svf_index* idx, const float* X, int64_t n, uint32_t* out_i
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t first = idx->n_alloc;
   CK(idx, put_rows(idx, X, first, n, st), "copy X");
-  s = insert_present_rows(idx, n, st);
+  s = insert_present_rows(idx, n, idx->p.insert_itopk, st);
   if (s != SVF_OK) return s;
   if (out_ids) {
     std::vector<uint32_t> h((size_t)n);

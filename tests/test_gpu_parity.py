@@ -258,6 +258,29 @@ def test_build_bit_exact_integer_data(svf, metric):
     assert np.array_equal(st["vec"], X)
 
 
+@pytest.mark.parametrize("metric", [0, 1])
+def test_build_itopk_then_insert_bit_exact(svf, metric):
+    """build_itopk (L_build, reading I15) drives svf_build's growth inserts only; later svf_insert calls use
+    insert_itopk.  Oracle: O5 at L_ins = L_build, then O3 at L_ins = L_insert on the result."""
+    gen = GLM(dim=32, ell=8, integer=True)
+    X = gen.rows(11, 11, 0, 5000) - (100.0 if metric else 0.0)
+    n0 = 4000
+    gr, er = oracle.build(X[:n0], R=24, seed_size=800, B_ins=500, L_ins=96, metric=metric)
+    idx = svf.Index.build(cuda(X[:n0]), degree=24, capacity=len(X), seed_size=800, insert_batch=500,
+                          insert_itopk=40, build_itopk=96, metric=metric)
+    st = idx.export()
+    assert np.array_equal(st["graph"][:n0], gr) and np.array_equal(st["edge_dist"][:n0], er)
+    G = np.vstack([gr, np.full((len(X) - n0, 24), SENT, np.uint32)])
+    E = np.vstack([er, np.full((len(X) - n0, 24), np.inf, np.float32)])
+    gi, ei = oracle.insert(X, G, E, n_alloc=n0, n_new=len(X) - n0, P=12, L_ins=40, B_ins=500, metric=metric)
+    idx.insert(cuda(X[n0:]))
+    st = idx.export()
+    assert np.array_equal(st["graph"], gi) and np.array_equal(st["edge_dist"], ei)
+    with pytest.raises(svf.SvfError) as e513:
+        svf.Index.build(cuda(X[:100]), degree=24, build_itopk=513)
+    assert e513.value.status == 1
+
+
 def test_build_tiny_and_padding(svf):
     X = np.array([[0.0], [1.0], [2.0], [3.0], [4.0]], np.float32)
     idx = svf.Index.build(X, degree=2)
