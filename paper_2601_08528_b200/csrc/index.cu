@@ -170,7 +170,9 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   // at small L (measured: C2 L=14, 1024 slots 9.9M QPS vs 2048 slots 9.5M vs 4096 slots 7.3M)
   // 2048 slots up to L = 128 (C3 10M x 96 at L = 96: 4.96 vs 5.40 ms with 4096 slots, C2 inserts at L = 128
   // 7.1 vs 7.2 ms; tools/param_sweep.py, tools/insert_rate.py)
-  const int autobits = L <= 16 ? 10 : (L <= 128 ? 11 : 13);
+  // 4096 slots for 128 < L <= 256 (C4 2M x 200, L_build 512: itopk 192 27.5 -> 15.4 ms, 256 37.6 -> 19.7 ms vs
+  // 8192 slots, identical results; 2048 slots is 2% faster again but recomputes 1.6x; profiles/c4_2m_hash.json)
+  const int autobits = L <= 16 ? 10 : (L <= 128 ? 11 : (L <= 256 ? 12 : 13));
   c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   if (c.hbits > 15) return why = "hash_bits too large", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);

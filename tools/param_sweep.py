@@ -25,12 +25,14 @@ def main():
     ap.add_argument("--width", default="1,2")
     ap.add_argument("--hash-bits", default="0,11")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--build-itopk", type=int, default=0)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     c = config_spec(a.config)
     n = a.n or c["n"]
     dev = torch.device("cuda:0")
-    idx = svf.Index.build(torch.from_numpy(base_rows(a.config, 0, n)).to(dev), degree=c["degree"], metric=c["metric"])
+    idx = svf.Index.build(torch.from_numpy(base_rows(a.config, 0, n)).to(dev), degree=c["degree"], metric=c["metric"],
+                          build_itopk=a.build_itopk)
     Q = torch.from_numpy(query_rows(a.config)).to(dev)
     gt = idx.knn_exact(Q, 10)[0].cpu().numpy()
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
