@@ -31,7 +31,7 @@ from workloads import base_rows, config_spec, query_rows  # noqa: E402
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
 BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
-L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 48, 64, 80, 96, 128, 192, 256]
+L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 40, 48, 64, 80, 96, 128, 192, 256]
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
