@@ -31,6 +31,9 @@ from workloads import base_rows, config_spec, query_rows  # noqa: E402
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
 BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
+# iteration caps tried (descending) at the chosen itopk; the smallest that keeps recall >= target is used (I4: a cap
+# ends a query's search early; 0 = run to convergence).  C2: cap 16 -> 17.5M QPS at 0.954 (profiles/c2_maxiter.json)
+MI_SWEEP = [64, 48, 40, 32, 28, 24, 20, 18, 16, 14, 12]
 L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 40, 48, 64, 80, 96, 128, 192, 256]
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -51,6 +54,7 @@ def parse():
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--itopk", type=int, default=0, help="fix itopk (skip the sweep)")
     ap.add_argument("--search-width", type=int, default=1)
+    ap.add_argument("--max-iter", type=int, default=-1, help="iteration cap (-1 = choose by recall, 0 = converge)")
     ap.add_argument("--build-itopk", type=int, default=-1, help="L_build (-1 = per-config default, 0 = insert_itopk)")
     ap.add_argument("--hash-bits", type=int, default=0, help="visited-table slots 2^b per query (0 = auto)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -231,6 +235,18 @@ def run_svf(a):
             L = L_SWEEP[-1]
     L = L or 16
     recall = next((s["recall"] for s in sweep if s["itopk"] == L), None)
+    MI = max(0, a.max_iter)
+    mi_sweep = []
+    if not a.ncu and a.max_iter < 0 and recall is not None and recall >= a.target_recall:
+        for cap in MI_SWEEP:
+            idx.set_search_params(a.search_width, 0, cap, a.hash_bits)
+            ids, d = sh.search(Qd, k, L)
+            rec = recall_at_k(ids.cpu().numpy(), gt, k)
+            mi_sweep.append({"max_iter": cap, "recall": round(rec, 4)})
+            if rec < a.target_recall:
+                break
+            MI, recall = cap, round(rec, 4)
+    idx.set_search_params(a.search_width, 0, MI, a.hash_bits)
 
     out_i = torch.empty((nq, k), dtype=torch.int32, device=dev)
     out_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
@@ -317,7 +333,7 @@ def run_svf(a):
     if D.world == 1 and D.rank == 0 and not a.ncu and not a.no_cpu:
         import oracle
 
-        cpu, cnt = cpu_baseline(oracle, idx.export(), Q, k, L, a.cpu_seconds)
+        cpu, cnt = cpu_baseline(oracle, idx.export(), Q, k, L, a.cpu_seconds, MI, a.search_width)
         alg = {"n_dist": float(cnt[:, 0].mean()), "n_exp": float(cnt[:, 1].mean()), "source": "oracle counters"}
         # SURVEY §8(d) counters beside QPS: recompute ratio (forgetful visited table), iterations GPU vs oracle
         gq = max(1, gpu_counters["queries"])
@@ -329,7 +345,8 @@ def run_svf(a):
                     "oracle_iters_per_query": round(float(cnt[:, 2].mean()), 3),
                     "iters_equal": bool(full and gpu_counters["iters"] == int(cnt[:, 2].sum())),
                     "oracle_sample_queries": int(len(cnt)),
-                    "max_iter_cap_hits": 0}              # bench searches to convergence (max_iter = 0, I4)
+                    "max_iter": MI,
+                    "max_iter_cap_hits": int((cnt[:, 2] >= MI).sum()) if MI else 0}
 
     # ---- inserts / deletes (I0-I3, D1) on 1% batches ---------------------------------------------------------------
     ins = None
@@ -366,7 +383,7 @@ def run_svf(a):
         idx.set_search_params(a.search_width, 0, 0, 13)   # 8192 slots: no forgetting at ~2K visits = unique distances
         sh.local.search(Qd, Lins, Lins)
         ic = idx.last_search_counters()
-        idx.set_search_params(a.search_width, 0, 0, a.hash_bits)
+        idx.set_search_params(a.search_width, 0, MI, a.hash_bits)
         nd_i, ne_i = ic["n_dist"] / max(1, ic["queries"]), ic["n_exp"] / max(1, ic["queries"])
         b_i = (nd_i * dim * 4 + ne_i * R * 4 + dim * 4 + Lins * 8) + Lins * R * 4 + 2 * R * (R * 8) + (dim * 4 + R * 8)
         ins_ms, del_ms = D.max(float(np.mean(t_ins))), D.max(float(np.mean(t_del)))
@@ -407,7 +424,8 @@ def run_svf(a):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-LM, integer-valued; DESIGN.md)",
             "config": {"workload": c["workload"], "n_per_gpu": n, "dim": dim, "degree": R, "batch": nq, "k": k,
-                       "itopk": L, "search_width": a.search_width, "build_itopk": build_L, "insert_itopk": 128, "recall_at_10": recall,
+                       "itopk": L, "search_width": a.search_width, "max_iter": MI, "max_iter_sweep": mi_sweep,
+                       "build_itopk": build_L, "insert_itopk": 128, "recall_at_10": recall,
                        "recall_sweep": sweep, "l2": "flushed between timed steps (256 MB write)",
                        "launch": "CUDA graph replay of svf_search" if graph is not None else "direct",
                        "parallelism": f"{D.world} shard(s), queries broadcast" +
@@ -424,28 +442,29 @@ def run_svf(a):
     D.close()
 
 
-def cpu_baseline(oracle, st, Q, k, L, seconds):
+def cpu_baseline(oracle, st, Q, k, L, seconds, max_iter=0, p=1):
     """Time oracle.graph_search (as it stands) on the exported graph with all host cores, bounded to ~seconds."""
     threads = os.cpu_count() or 1
     X, G = st["vec"], st["graph"]
     tomb = st["tomb"] if st["tomb"].any() else None
     probe = Q[:256]
     t0 = time.perf_counter()
-    oracle.graph_search(X, G, probe, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+    oracle.graph_search(X, G, probe, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads, max_iter=max_iter, p=p)
     per_q = (time.perf_counter() - t0) / len(probe)
     nq_s = int(min(len(Q), max(256, seconds / max(per_q, 1e-9))))
     sample = Q[:nq_s]
     t0 = time.perf_counter()
-    _, _, cnt = oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+    _, _, cnt = oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads,
+                                    max_iter=max_iter, p=p)
     dt = time.perf_counter() - t0
     reps = 1
     while dt * (reps + 1) / reps < seconds and reps < 50 and nq_s == len(Q):
         t1 = time.perf_counter()
-        oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads)
+        oracle.graph_search(X, G, sample, k, L, tomb=tomb, n_alloc=st["n_alloc"], threads=threads, max_iter=max_iter, p=p)
         dt += time.perf_counter() - t1
         reps += 1
     return ({"value": round(nq_s * reps / dt, 1), "unit": "queries/s", "cores": threads, "kind": "oracle",
-             "sample": f"{nq_s} queries x {reps} pass(es) at itopk={L} on the exported GPU-built graph "
+             "sample": f"{nq_s} queries x {reps} pass(es) at itopk={L}, width={p}, max_iter={max_iter} on the exported GPU-built graph "
                        f"(oracle graph_search_ref, std::thread x {threads})"}, cnt)
 
 
@@ -485,8 +504,17 @@ def run_reference(a):
             L = Ls
             break
     L = L or L_SWEEP[-1]
+    MI, mi_sweep = max(0, a.max_iter), []
+    if a.max_iter < 0 and sweep[-1]["recall"] >= a.target_recall:     # same cap selection as the svf arm
+        for cap in MI_SWEEP:
+            ids, _, _ = oracle.graph_search(st["vec"], st["graph"], probe, k, L, max_iter=cap, threads=threads)
+            rec = recall_at_k(ids.astype(np.int64).astype(np.int32), gt[:1000], k)
+            mi_sweep.append({"max_iter": cap, "recall": round(rec, 4)})
+            if rec < a.target_recall:
+                break
+            MI = cap
     t0 = time.perf_counter()
-    oracle.graph_search(st["vec"], st["graph"], Q[:256], k, L, threads=threads)
+    oracle.graph_search(st["vec"], st["graph"], Q[:256], k, L, threads=threads, max_iter=MI)
     per_q = (time.perf_counter() - t0) / 256
     budget = 150.0 / max(1, a.steps + a.warmup)
     m = int(min(nq, max(64, budget / max(per_q, 1e-9))))
@@ -495,7 +523,7 @@ def run_reference(a):
         s0 = (i * m) % nq
         sample = np.roll(Q, -s0, axis=0)[:m]
         t1 = time.perf_counter()
-        oracle.graph_search(st["vec"], st["graph"], sample, k, L, threads=threads)
+        oracle.graph_search(st["vec"], st["graph"], sample, k, L, threads=threads, max_iter=MI)
         if i >= a.warmup:
             times.append(time.perf_counter() - t1)
     ms = 1e3 * float(np.mean(times))
@@ -504,10 +532,10 @@ def run_reference(a):
             "value": round(qps, 1), "unit": "queries/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64-accumulate (fp32 decisions)", "data": "synthetic (seeded G-LM, integer-valued)",
-            "config": {"workload": c["workload"], "n_per_gpu": n, "batch": nq, "k": k, "itopk": L, "build_itopk": build_L,
+            "config": {"workload": c["workload"], "n_per_gpu": n, "batch": nq, "k": k, "itopk": L, "max_iter": MI, "max_iter_sweep_1000q": mi_sweep, "build_itopk": build_L,
                        "recall_sweep_1000q": sweep, "step_sample_queries": m},
             "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{m} queries per step at itopk={L}"},
+                             "sample": f"{m} queries per step at itopk={L}, max_iter={MI}"},
             "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
