@@ -21,7 +21,8 @@ def c2():
     X = base_rows("C2")
     Q = query_rows("C2")
     Xnew = base_rows("C2", 1_000_000, 10_000)
-    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, capacity=1_010_000)
+    # bench.py's build: L_build = BUILD_ITOPK["C2"] = 256, streamed inserts at insert_itopk = 128
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, capacity=1_010_000, build_itopk=256)
     return svf, idx, X, Q, Xnew
 
 
@@ -48,14 +49,19 @@ def test_c2_graph_invariants(c2):
     assert indeg.sum() == g.size and (indeg == 0).mean() < 0.02
 
 
-@pytest.mark.parametrize("L", [14, 32])
-def test_c2_search_sampled_bit_exact(c2, L):
+@pytest.mark.parametrize("L,cap", [(10, 16), (10, 0), (14, 0), (32, 0)])
+def test_c2_search_sampled_bit_exact(c2, L, cap):
+    """(10, 16) is the bench headline launch: itopk 10 with the iteration cap its sweep picks."""
     svf, idx, X, Q, _ = c2
-    ids, d = idx.search(torch.from_numpy(Q).cuda(), 10, L)
+    idx.set_search_params(1, 0, cap, 0)
+    try:
+        ids, d = idx.search(torch.from_numpy(Q).cuda(), 10, L)
+    finally:
+        idx.set_search_params(1, 0, 0, 0)
     ids, d = u32(ids), d.cpu().numpy()
     st = idx.export()
-    sample = np.random.default_rng(L).choice(len(Q), 400, replace=False)
-    ri, rd, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, qidx=sample)
+    sample = np.random.default_rng(L + cap).choice(len(Q), 400, replace=False)
+    ri, rd, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, max_iter=cap, qidx=sample)
     assert np.array_equal(ids[sample], ri) and np.array_equal(d[sample], rd)
 
 
@@ -101,7 +107,7 @@ def c3():
 
     X = base_rows("C3")
     Q = query_rows("C3", 2000)
-    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64)
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, build_itopk=256)   # bench.py's C3 build
     return svf, idx, X, Q
 
 
@@ -115,10 +121,13 @@ def test_c3_float_search_and_knn_sampled(c3):
     np.testing.assert_allclose(gd[:12], rd, rtol=1e-4, atol=1e-6)
     mism = gi[:12] != ri
     assert np.all(np.abs(gd[:12][mism] - rd[mism]) <= 1e-5 * np.abs(rd[mism]) + 1e-7)
-    for L in (32, 96):
+    for L, p, cap in ((32, 1, 0), (96, 1, 0), (32, 2, 0), (40, 1, 48)):   # (32, 2) / (40, 1, cap 48): bench picks
+        idx.set_search_params(p, 0, cap, 0)
         ids, d = idx.search(torch.from_numpy(Q[sample]).cuda(), 10, L)
+        idx.set_search_params(1, 0, 0, 0)
         ids, d = u32(ids), d.cpu().numpy()
-        oi, od, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, qidx=np.arange(300))
+        oi, od, _ = oracle.graph_search(st["vec"], st["graph"], Q[sample], 10, L, p=p, max_iter=cap,
+                                        qidx=np.arange(300))
         r_gpu, r_orc = oracle.recall_ids(ids, gi, 10), oracle.recall_ids(oi, gi, 10)
         assert abs(r_gpu - r_orc) <= 0.005, (L, r_gpu, r_orc)
         same = ids == oi
