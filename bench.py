@@ -34,6 +34,12 @@ BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
 # iteration caps tried (descending) at the chosen itopk; the smallest that keeps recall >= target is used (I4: a cap
 # ends a query's search early; 0 = run to convergence).  C2: cap 16 -> 17.5M QPS at 0.954 (profiles/c2_maxiter.json)
 MI_SWEEP = [64, 48, 40, 32, 28, 24, 20, 18, 16, 14, 12]
+
+
+def mi_caps(L: int) -> list:
+    """Caps to try at itopk L, descending: MI_SWEEP plus multiples of L (large pools need ~L iterations)."""
+    return sorted(set(MI_SWEEP) | {int(L * f) for f in (3, 2.5, 2, 1.75, 1.5, 1.25, 1.1)}, reverse=True)
+
 L_SWEEP = [10, 11, 12, 13, 14, 16, 20, 24, 32, 40, 48, 64, 80, 96, 128, 192, 256]
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -238,7 +244,7 @@ def run_svf(a):
     MI = max(0, a.max_iter)
     mi_sweep = []
     if not a.ncu and a.max_iter < 0 and recall is not None and recall >= a.target_recall:
-        for cap in MI_SWEEP:
+        for cap in mi_caps(L):
             idx.set_search_params(a.search_width, 0, cap, a.hash_bits)
             ids, d = sh.search(Qd, k, L)
             rec = recall_at_k(ids.cpu().numpy(), gt, k)
@@ -506,7 +512,7 @@ def run_reference(a):
     L = L or L_SWEEP[-1]
     MI, mi_sweep = max(0, a.max_iter), []
     if a.max_iter < 0 and sweep[-1]["recall"] >= a.target_recall:     # same cap selection as the svf arm
-        for cap in MI_SWEEP:
+        for cap in mi_caps(L):
             ids, _, _ = oracle.graph_search(st["vec"], st["graph"], probe, k, L, max_iter=cap, threads=threads)
             rec = recall_at_k(ids.astype(np.int64).astype(np.int32), gt[:1000], k)
             mi_sweep.append({"max_iter": cap, "recall": round(rec, 4)})
