@@ -31,6 +31,10 @@ from workloads import base_rows, config_spec, query_rows  # noqa: E402
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
 BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
+# L_insert per config (svf_params.insert_itopk; default 128).  C2 on the L_build-256 graph: 64 inserts 1.86x
+# faster with recall@10 after 120K inserts 0.9645 vs 0.9666 at 128 (profiles/insert_knobs.jsonl); the bench line
+# carries recall after its own insert/delete rounds ("recall_after_updates").
+INSERT_ITOPK = {"C2": 64}
 # iteration caps tried (descending) at the chosen itopk; the smallest that keeps recall >= target is used (I4: a cap
 # ends a query's search early; 0 = run to convergence).  C2: cap 16 -> 17.5M QPS at 0.954 (profiles/c2_maxiter.json)
 MI_SWEEP = [64, 48, 40, 32, 28, 24, 20, 18, 16, 14, 12]
@@ -62,6 +66,7 @@ def parse():
     ap.add_argument("--search-width", type=int, default=1)
     ap.add_argument("--max-iter", type=int, default=-1, help="iteration cap (-1 = choose by recall, 0 = converge)")
     ap.add_argument("--build-itopk", type=int, default=-1, help="L_build (-1 = per-config default, 0 = insert_itopk)")
+    ap.add_argument("--insert-itopk", type=int, default=-1, help="L_insert (-1 = per-config default)")
     ap.add_argument("--hash-bits", type=int, default=0, help="visited-table slots 2^b per query (0 = auto)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -193,9 +198,11 @@ def run_svf(a):
     Qd = torch.from_numpy(Q).to(dev)
     torch.cuda.synchronize()
     build_L = a.build_itopk if a.build_itopk >= 0 else BUILD_ITOPK.get(a.config, 0)
+    ins_L = a.insert_itopk if a.insert_itopk > 0 else INSERT_ITOPK.get(a.config, 128)
     t0 = time.time()
     idx = svf.Index.build(Xd, degree=R, metric=c["metric"], capacity=n + (0 if Xnew is None else len(Xnew)),
-                          device=D.dev.index, search_width=a.search_width, build_itopk=build_L)
+                          device=D.dev.index, search_width=a.search_width, build_itopk=build_L,
+                          insert_itopk=ins_L)
     torch.cuda.synchronize()
     t_build = time.time() - t0
     del Xd
@@ -385,7 +392,7 @@ def run_svf(a):
             t_del.append(e0.elapsed_time(e1))
         # algorithmic bytes per insert: B_i = B_q(L_insert) + |C| R 4 + 2 R (R 8) + (D 4 + R 8), with the
         # L_insert = 128 search's counters measured by an itopk-128 search over the same index (GPU counters)
-        Lins = 128
+        Lins = ins_L
         idx.set_search_params(a.search_width, 0, 0, 13)   # 8192 slots: no forgetting at ~2K visits = unique distances
         sh.local.search(Qd, Lins, Lins)
         ic = idx.last_search_counters()
@@ -393,18 +400,25 @@ def run_svf(a):
         nd_i, ne_i = ic["n_dist"] / max(1, ic["queries"]), ic["n_exp"] / max(1, ic["queries"])
         b_i = (nd_i * dim * 4 + ne_i * R * 4 + dim * 4 + Lins * 8) + Lins * R * 4 + 2 * R * (R * 8) + (dim * 4 + R * 8)
         ins_ms, del_ms = D.max(float(np.mean(t_ins))), D.max(float(np.mean(t_del)))
+        rau = None
+        if gt is not None:     # search quality after the update rounds: fresh ground truth over the live set
+            gt2 = sh.knn_exact(Qd, k)[0].cpu().numpy()
+            rau = round(recall_at_k(sh.search(Qd, k, L)[0].cpu().numpy(), gt2, k), 4)
         ins = {"inserts_per_s": round(ins_batch * D.world / (ins_ms / 1e3), 1),
                "deletes_per_s": round(ins_batch * D.world / (del_ms / 1e3), 1),
                "batch": ins_batch, "ms_per_insert_batch": round(ins_ms, 3), "ms_per_delete_batch": round(del_ms, 3),
                "insert_breakdown_ms": {kk: round(v[0] / max(1, ins_warm + ins_steps), 3)
                                        for kk, v in iprof.items() if kk != "search"},
-               "build_inserts_per_s": round(n / t_build, 1)}
+               "build_inserts_per_s": round(n / t_build, 1),
+               "recall_after_updates": rau,
+               "updates": f"{ins_warm + ins_steps} insert batches + {ins_steps} delete batches of {ins_batch} "
+                          f"(L_insert {ins_L}), then the timed search (itopk {L}, cap {MI}) vs fresh exact kNN"}
         pk = measured_peaks().get("hbm_gbs", 6650.0)
         ach = ins_batch / (ins_ms / 1e3) * b_i / 1e9
         ins["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s",
                            "frac": round(ach / pk, 4), "alg_bytes_per_insert": round(b_i, 1),
                            "alg_counts": {"n_dist": round(nd_i, 2), "n_exp": round(ne_i, 2),
-                                          "source": "GPU counters of an itopk-128 search over the same index with "
+                                          "source": f"GPU counters of an itopk-{Lins} search over the same index with "
                                                     "an 8192-slot visited table (no forgetting: unique distances)"}}
 
     if alg is None:
@@ -431,7 +445,7 @@ def run_svf(a):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-LM, integer-valued; DESIGN.md)",
             "config": {"workload": c["workload"], "n_per_gpu": n, "dim": dim, "degree": R, "batch": nq, "k": k,
                        "itopk": L, "search_width": a.search_width, "max_iter": MI, "max_iter_sweep": mi_sweep,
-                       "build_itopk": build_L, "insert_itopk": 128, "recall_at_10": recall,
+                       "build_itopk": build_L, "insert_itopk": ins_L, "recall_at_10": recall,
                        "recall_sweep": sweep, "l2": "flushed between timed steps (256 MB write)",
                        "launch": "CUDA graph replay of svf_search" if graph is not None else "direct",
                        "parallelism": f"{D.world} shard(s), queries broadcast" +
