@@ -31,10 +31,11 @@ from workloads import base_rows, config_spec, query_rows  # noqa: E402
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
 BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
-# L_insert per config (svf_params.insert_itopk; default 128).  C2 on the L_build-256 graph: 64 inserts 1.86x
-# faster with recall@10 after 120K inserts 0.9645 vs 0.9666 at 128 (profiles/insert_knobs.jsonl); the bench line
-# carries recall after its own insert/delete rounds ("recall_after_updates").
-INSERT_ITOPK = {"C2": 64}
+# L_insert per config (svf_params.insert_itopk; default 128).  Not lowered to 64 for C2 although that inserts
+# 1.86x faster with recall after 120K inserts within 0.002 (profiles/insert_knobs.jsonl): at L_insert <= R the
+# detour selection keeps every candidate (no pruning), rows drift toward a plain kNN graph, and a consolidation that
+# rebuilds rows from a 64-entry candidate list collapsed C2 recall to 0.27 (profiles/r01_bench_c2_ins64_cons.json).
+INSERT_ITOPK: dict = {}
 # iteration caps tried (descending) at the chosen itopk; the smallest that keeps recall >= target is used (I4: a cap
 # ends a query's search early; 0 = run to convergence).  C2: cap 16 -> 17.5M QPS at 0.954 (profiles/c2_maxiter.json)
 MI_SWEEP = [64, 48, 40, 32, 28, 24, 20, 18, 16, 14, 12]
@@ -400,17 +401,35 @@ def run_svf(a):
         nd_i, ne_i = ic["n_dist"] / max(1, ic["queries"]), ic["n_exp"] / max(1, ic["queries"])
         b_i = (nd_i * dim * 4 + ne_i * R * 4 + dim * 4 + Lins * 8) + Lins * R * 4 + 2 * R * (R * 8) + (dim * 4 + R * 8)
         ins_ms, del_ms = D.max(float(np.mean(t_ins))), D.max(float(np.mean(t_del)))
-        rau = None
+        rau, rau_rep, rep = None, None, None
         if gt is not None:     # search quality after the update rounds: fresh ground truth over the live set
             gt2 = sh.knn_exact(Qd, k)[0].cpu().numpy()
             rau = round(recall_at_k(sh.search(Qd, k, L)[0].cpu().numpy(), gt2, k), 4)
+            # then the paper's localized repair of vertices with > 50% deleted neighbours (NEXT-1)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rs = idx.repair()
+            e1.record()
+            torch.cuda.synchronize()
+            rep = {"ms": round(D.max(e0.elapsed_time(e1)), 3), **{kk: v for kk, v in rs.items() if kk != "hist"}}
+            rau_rep = round(recall_at_k(sh.search(Qd, k, L)[0].cpu().numpy(), gt2, k), 4)
+            # and the global consolidation (NEXT-4): every neighbourhood with a deleted member rebuilt
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ncons = idx.consolidate()
+            e1.record()
+            torch.cuda.synchronize()
+            rep["consolidation"] = {"ms": round(D.max(e0.elapsed_time(e1)), 3), "rewritten": int(ncons),
+                                    "recall_after": round(recall_at_k(sh.search(Qd, k, L)[0].cpu().numpy(), gt2,
+                                                                      k), 4)}
         ins = {"inserts_per_s": round(ins_batch * D.world / (ins_ms / 1e3), 1),
                "deletes_per_s": round(ins_batch * D.world / (del_ms / 1e3), 1),
                "batch": ins_batch, "ms_per_insert_batch": round(ins_ms, 3), "ms_per_delete_batch": round(del_ms, 3),
                "insert_breakdown_ms": {kk: round(v[0] / max(1, ins_warm + ins_steps), 3)
                                        for kk, v in iprof.items() if kk != "search"},
                "build_inserts_per_s": round(n / t_build, 1),
-               "recall_after_updates": rau,
+               "recall_after_updates": rau, "repair": rep, "recall_after_repair": rau_rep,
                "updates": f"{ins_warm + ins_steps} insert batches + {ins_steps} delete batches of {ins_batch} "
                           f"(L_insert {ins_L}), then the timed search (itopk {L}, cap {MI}) vs fresh exact kNN"}
         pk = measured_peaks().get("hbm_gbs", 6650.0)

@@ -21,8 +21,8 @@ def c2():
     X = base_rows("C2")
     Q = query_rows("C2")
     Xnew = base_rows("C2", 1_000_000, 10_000)
-    # bench.py's build: L_build = BUILD_ITOPK["C2"] = 256, streamed inserts at INSERT_ITOPK["C2"] = 64
-    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, capacity=1_010_000, build_itopk=256, insert_itopk=64)
+    # bench.py's build: L_build = BUILD_ITOPK["C2"] = 256, streamed inserts at insert_itopk = 128
+    idx = svf.Index.build(torch.from_numpy(X).cuda(), degree=64, capacity=1_010_000, build_itopk=256)
     return svf, idx, X, Q, Xnew
 
 
@@ -88,7 +88,7 @@ def test_c2_insert_and_delete_whole_graph_bit_exact(c2):
     G = np.vstack([st0["graph"], np.full((len(Xnew), 64), SENT, np.uint32)])
     E = np.vstack([st0["edge_dist"], np.full((len(Xnew), 64), np.inf, np.float32)])
     Xall = np.vstack([X, Xnew])
-    gr, er = oracle.insert(Xall, G, E, n_alloc=n0, n_new=len(Xnew), P=32, L_ins=64, B_ins=4096,
+    gr, er = oracle.insert(Xall, G, E, n_alloc=n0, n_new=len(Xnew), P=32, L_ins=128, B_ins=4096,
                            tomb=pack_tomb(dead, cap))
     assert np.array_equal(st1["graph"], gr)
     assert np.array_equal(st1["edge_dist"], er)
