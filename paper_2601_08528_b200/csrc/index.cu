@@ -879,7 +879,8 @@ static svf_status repair_impl(svf_index* idx, int c, double threshold, int64_t* 
   CK(idx, launch_repair_mark(idx->graph, tomb, idx->R, idx->n_alloc, threshold, idx->scratch, st, &n_list, h),
      "repair mark");
   if (n_list > 0) {
-    const int cap = idx->p.insert_itopk;  // U is cut to an insertion-sized candidate list (reading R1')
+    int cap = idx->p.insert_itopk;  // U is cut to an insertion-sized candidate list (reading R1')
+    if (const char* v = getenv("SVF_REPAIR_CAP")) cap = std::max(1, std::min(512, atoi(v)));  // experiment hook
     const size_t bytes = repair_apply_scratch_bytes(n_list, idx->R, cap);
     void* sp = nullptr;
     CK(idx, cudaMallocAsync(&sp, bytes, st), "repair apply scratch");
