@@ -30,7 +30,7 @@ from workloads import base_rows, config_spec, query_rows  # noqa: E402
 # L_build per config (svf_params.build_itopk; reading I15): the graph is grown once at this candidate-list size, then
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10 (0.956 needed itopk 14 at 128); C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
-BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 256, "C4": 512, "C5": 256}
+BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 512, "C4": 512, "C5": 512}
 # L_insert per config (svf_params.insert_itopk; default 128).  Not lowered to 64 for C2 although that inserts
 # 1.86x faster with recall after 120K inserts within 0.002 (profiles/insert_knobs.jsonl): at L_insert <= R the
 # detour selection keeps every candidate (no pruning), rows drift toward a plain kNN graph, and a consolidation that
