@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--build-itopk", type=int, default=0)
     ap.add_argument("--max-iter", default="0")
+    ap.add_argument("--n-init", default="0", help="random entry points (0 = itopk)")
     ap.add_argument("--handoff", default="-1", help="pair-mode handoff thresholds %% (-1 = auto, 0 = off)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -41,10 +42,10 @@ def main():
     oi = torch.empty((len(Q), 10), dtype=torch.int32, device=dev)
     od = torch.empty((len(Q), 10), dtype=torch.float32, device=dev)
     rows = []
-    for L, p, hb, mi, ho in itertools.product(*[[int(x) for x in v.split(",")]
-                                               for v in (a.itopk, a.width, a.hash_bits, a.max_iter, a.handoff)]):
+    for L, p, hb, mi, ho, ni in itertools.product(*[[int(x) for x in v.split(",")] for v in
+                                                   (a.itopk, a.width, a.hash_bits, a.max_iter, a.handoff, a.n_init)]):
         try:
-            idx.set_search_params(p, 0, mi, hb)
+            idx.set_search_params(p, ni, mi, hb)
             idx.set_search_handoff(ho)
             idx.search_into(Q, 10, L, oi, od)
         except Exception as e:  # noqa: BLE001 (invalid combinations are reported, not fatal)
@@ -66,7 +67,7 @@ def main():
         ids = oi.cpu().numpy()
         rec = float((ids[:, :, None] == gt[:, None, :]).any(axis=2).sum()) / ids.size
         cnt = idx.last_search_counters()
-        r = {"itopk": L, "width": p, "hash_bits": hb, "max_iter": mi, "handoff": ho, "median_ms": round(float(np.median(ts)), 4),
+        r = {"itopk": L, "width": p, "hash_bits": hb, "max_iter": mi, "handoff": ho, "n_init": ni, "median_ms": round(float(np.median(ts)), 4),
              "qps": round(len(Q) / (np.median(ts) * 1e-3)), "recall": round(rec, 4),
              "n_dist": round(cnt["n_dist"] / max(1, cnt["queries"]), 1),
              "iters": round(cnt["iters"] / max(1, cnt["queries"]), 2)}
