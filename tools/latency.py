@@ -22,9 +22,12 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--batches", default="1,8,64,256,1024,4096")
     ap.add_argument("--out", default="")
+    ap.add_argument("--build-itopk", type=int, default=0)
+    ap.add_argument("--max-iter", type=int, default=0)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    idx = svf.Index.build(torch.from_numpy(base_rows("C2")).to(dev), degree=64)
+    idx = svf.Index.build(torch.from_numpy(base_rows("C2")).to(dev), degree=64, build_itopk=a.build_itopk)
+    idx.set_search_params(1, 0, a.max_iter, 0)
     Q = torch.from_numpy(query_rows("C2")).to(dev)
     res = []
     for b in [int(x) for x in a.batches.split(",")]:

@@ -24,13 +24,16 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--searches", type=int, default=1, help="search batches per insert batch")
     ap.add_argument("--out", default="")
+    ap.add_argument("--build-itopk", type=int, default=0)
+    ap.add_argument("--max-iter", type=int, default=0)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     n, nb = 1_000_000, 10_000
     X = torch.from_numpy(base_rows("C2")).to(dev)
     Xn = torch.from_numpy(base_rows("C2", n, nb * (3 * a.reps + 2))).to(dev)
     Q = torch.from_numpy(query_rows("C2")).to(dev)
-    idx = svf.Index.build(X, degree=64, capacity=n + len(Xn))
+    idx = svf.Index.build(X, degree=64, capacity=n + len(Xn), build_itopk=a.build_itopk)
+    idx.set_search_params(1, 0, a.max_iter, 0)
     s_q, s_u = torch.cuda.Stream(), torch.cuda.Stream()
     k, L = 10, a.itopk
     used = [0]
