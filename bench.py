@@ -327,11 +327,11 @@ def run_svf(a):
         Qh = torch.from_numpy(Q).pin_memory()
         oi_h = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)   # pinned result buffers, reused
         od_h = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
-        for _ in range(max(10, a.warmup // 2)):
+        for _ in range(max(20, a.warmup)):
             idx.search_into(Qh, k, L, oi_h, od_h)
         D.barrier()
         tt = []
-        for _ in range(max(30, a.steps // 2)):
+        for _ in range(max(60, a.steps // 2)):
             flush.zero_()
             torch.cuda.synchronize()
             t1 = time.perf_counter()
