@@ -124,11 +124,13 @@ svf_status svf_knn_exact(svf_index* idx, const float* Q, int64_t nq, int32_t k, 
 svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_repaired, uint64_t hist[5],
                       void* stream);
 
-/* Global consolidation (reading C1 in DESIGN.md): "a global consolidation of all
- * affected neighborhoods by aggregating candidates from the outgoing neighbors of deleted vertices" — every live
- * vertex with at least one deleted neighbour is rebuilt as by svf_repair with c = degree (all live members of each
- * deleted neighbour's list) and threshold 0.  Afterwards no live row references a deleted vertex.  *n_rewritten
- * (nullable) = rows rewritten.  Synchronous; may overlap an svf_search on another stream (see svf_search). */
+/* Global consolidation (reading C2 in DESIGN.md): "a global consolidation of all affected
+ * neighborhoods by aggregating candidates from the outgoing neighbors of deleted vertices".  Every live row holding a
+ * tombstoned id keeps its live entries (prefix entries in their slots) and refills its vacancies from the live
+ * members of its deleted neighbours' lists: a deleted prefix slot takes the nearest member of that deleted
+ * neighbour's own list, the tail vacancies take the nearest of the remaining union; the tail is re-sorted by
+ * (edge_dist, id).  Afterwards no live row references a deleted vertex.  *n_rewritten (nullable) = rows rewritten.
+ * Synchronous; may overlap an svf_search on another stream (see svf_search). */
 svf_status svf_consolidate(svf_index* idx, int64_t* n_rewritten, void* stream);
 
 /* Automatic consolidation: after an svf_delete, when the vertices deleted since the last consolidation exceed
@@ -143,6 +145,22 @@ svf_status svf_consolidation_stats(svf_index* idx, int64_t out[2]);
  * per query (the step after the NCCL all-gather).  Uses the current device. */
 svf_status svf_merge_topk(const uint32_t* ids, const float* dists, int32_t G, int64_t nq, int32_t k,
                           uint32_t* out_ids, float* out_dists, void* stream);
+
+/* Sharded search, SURVEY §8(e) (the dataset is split into n_logical shards, global id g -> shard g mod n_logical,
+ * local id g div n_logical; a rank holds several shards).  Step 2, a rank's pre-merge: merge n_lists (<= 16) shard
+ * results ids/dists [n_lists][nq][k] (device, LOCAL ids, SVF_SENTINEL padded) into the first k per query by
+ * (dist, id) with GLOBAL ids g = local * n_logical + shard[i] (shard: HOST array of n_lists values < n_logical),
+ * written to out_pairs[nq][k] (device) as packed u64 pairs (float bits of the distance << 32 | global id; padding
+ * = (+inf, SVF_SENTINEL)), ready for one all_gather_into_tensor.  Global ids must stay below 2^31.  Uses the current
+ * device; INVALID on bad sizes or non-device buffers. */
+svf_status svf_shard_premerge(const uint32_t* ids, const float* dists, int32_t n_lists, int64_t nq, int32_t k,
+                              uint32_t n_logical, const uint32_t* shard, uint64_t* out_pairs, void* stream);
+
+/* Step 4: merge G gathered pair lists pairs[G][nq][k] (device, as written by svf_shard_premerge) into out_ids /
+ * out_dists [nq][k] (device), the first k per query by (dist, id).  Merging is associative over this total order, so
+ * the result does not depend on how the shards were grouped into ranks. */
+svf_status svf_merge_pairs(const uint64_t* pairs, int32_t G, int64_t nq, int32_t k, uint32_t* out_ids,
+                           float* out_dists, void* stream);
 
 /* Copy the index state out (any pointer may be NULL to skip): vec[n_alloc][dim] (unpadded), graph[n_alloc][R],
  * edge_dist[n_alloc][R], tomb[ceil(n_alloc/32)], *n_alloc.  Synchronous. */

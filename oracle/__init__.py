@@ -42,6 +42,7 @@ def lib():
         L.orc_insert.argtypes = [P, I, I, P, P, P, I, I, I64, I64, I, I, I, I, I, U64, I]
         L.orc_build.argtypes = [P, I64, I, I, I, I, I, I, I, I, I, I, U64, P, P, I]
         L.orc_merge_topk.argtypes = [P, P, I, I64, I, P, P]
+        L.orc_consolidate.argtypes = [P, I, I, P, P, P, I, I, I64, P]
         L.orc_repair.argtypes = [P, I, I, P, P, P, I, I, I64, I, ctypes.c_double, I, P, P]
         L.orc_repair_mode.argtypes = [P, I, I, P, P, P, I, I, I64, I, ctypes.c_double, I, I, P, P]
         _lib = L
@@ -183,14 +184,37 @@ def repair(X, graph, edge_dist, tomb, c: int = 8, threshold: float = 0.5, metric
     return graph, edge_dist, nrep.value, hist
 
 
-def consolidate(X, graph, edge_dist, tomb, metric: int = 0, n_alloc: Optional[int] = None, P: Optional[int] = None,
-                cap: int = 128):
+def consolidate(X, graph, edge_dist, tomb, metric: int = 0, n_alloc: Optional[int] = None, P: Optional[int] = None):
     """NEXT-4 global consolidation ("aggregating candidates from the outgoing neighbors of deleted
-    vertices"; reading C1): orc_repair with c = R (every live member of each deleted neighbour's list) and
-    threshold 0 (every live vertex with a deleted neighbour).  Returns (graph, edge_dist, n_rewritten)."""
-    R = np.asarray(graph).shape[1]
-    g, e, n, _ = repair(X, graph, edge_dist, tomb, c=R, threshold=0.0, metric=metric, n_alloc=n_alloc, P=P, cap=cap)
-    return g, e, n
+    vertices"; reading C2): every live row with a tombstoned entry keeps its live entries in place and refills its
+    vacancies from the live members of the deleted neighbours' lists (a deleted prefix slot from its own deleted
+    neighbour's list, the tail vacancies by the nearest of the rest).  Returns (graph, edge_dist, n_rewritten)."""
+    X, tomb = _f32(X), _u32(tomb)
+    graph = np.array(graph, dtype=np.uint32, copy=True, order="C")
+    edge_dist = np.array(edge_dist, dtype=np.float32, copy=True, order="C")
+    n_alloc = graph.shape[0] if n_alloc is None else n_alloc
+    R = graph.shape[1]
+    n = ctypes.c_int64()
+    rc = lib().orc_consolidate(_p(X), X.shape[1], metric, _p(graph), _p(edge_dist), _p(tomb), R,
+                               R // 2 if P is None else P, n_alloc, ctypes.byref(n))
+    assert rc == 0
+    return graph, edge_dist, n.value
+
+
+def delete(tomb, ids, n_alloc: int):
+    """O4 lazy deletion: set the tombstone bit of each id on a copy of the bitset.  Idempotent.
+    Returns (tomb, n_newly_deleted); raises KeyError (nothing deleted) if any id >= n_alloc."""
+    t = np.array(tomb, dtype=np.uint32, copy=True)
+    ids = [int(i) for i in np.asarray(ids).ravel()]
+    if any(i < 0 or i >= n_alloc for i in ids):
+        raise KeyError("delete of an id >= n_alloc")
+    newly = 0
+    for i in ids:
+        w, b = i >> 5, i & 31
+        if not (int(t[w]) >> b) & 1:
+            t[w] = np.uint32(int(t[w]) | (1 << b))
+            newly += 1
+    return t, newly
 
 
 def merge_topk(ids, d):

@@ -476,6 +476,98 @@ int orc_repair_mode(const float* X, int D, int metric, uint32_t* graph, float* e
   return 0;
 }
 
+// NEXT-4: global consolidation ("a global consolidation of all affected neighborhoods by aggregating
+// candidates from the outgoing neighbors of deleted vertices"), reading C2 in DESIGN.md.  For every live v < n_alloc
+// whose row holds at least one vacant entry (a tombstoned id), with all rows read from the call's starting state:
+//   * live entries stay where they are (the protected prefix keeps its slots, the live tail entries are kept);
+//   * U = live members of N_out(p) over the tombstoned p of row(v) (slot order), excluding v and the live entries of
+//     row(v), without duplicates, each with its distance to v;
+//   * each tombstoned PREFIX slot s (slot order) is refilled by the nearest (dist, id) member of N_out(p_s) in U not
+//     taken by an earlier slot (the two-hop edge through the deleted p_s);
+//   * the m tail vacancies (tombstoned tail entries plus empty tail slots) are refilled by the m nearest members of U
+//     not taken by the prefix; the tail (kept live entries + refills) is re-sorted by key(d, id), empty slots last.
+// A vacancy with no eligible candidate becomes an empty slot (sentinel, +inf).  Afterwards no live row references a
+// deleted vertex; rows of deleted vertices and rows without deleted neighbours are unchanged.
+int orc_consolidate(const float* X, int D, int metric, uint32_t* graph, float* edge_dist, const uint32_t* tomb, int R,
+                    int P, int64_t n_alloc, int64_t* n_rewritten) {
+  if (P < 0 || P > R) return 1;
+  std::vector<uint32_t> snap(graph, graph + (size_t)n_alloc * R);
+  std::vector<float> snapd(edge_dist, edge_dist + (size_t)n_alloc * R);
+  int64_t rewritten = 0;
+  for (int64_t v = 0; v < n_alloc; ++v) {
+    if (dead(tomb, (uint32_t)v)) continue;
+    const uint32_t* row = snap.data() + (size_t)v * R;
+    const float* rowd = snapd.data() + (size_t)v * R;
+    bool affected = false;
+    std::unordered_set<uint32_t> in_row;
+    for (int s = 0; s < R; ++s) {
+      if (row[s] == SENT) continue;
+      if (dead(tomb, row[s])) affected = true;
+      else in_row.insert(row[s]);
+    }
+    if (!affected) continue;
+    // U with distances (first occurrence order is irrelevant: every choice below is by (dist, id))
+    std::vector<Entry> U;
+    std::unordered_set<uint32_t> seen;
+    for (int s = 0; s < R; ++s) {
+      const uint32_t p = row[s];
+      if (p == SENT || !dead(tomb, p)) continue;
+      for (int t = 0; t < R; ++t) {
+        const uint32_t x = snap[(size_t)p * R + t];
+        if (x == SENT || dead(tomb, x) || x == (uint32_t)v || in_row.count(x) || seen.count(x)) continue;
+        seen.insert(x);
+        U.push_back({dist(X + (size_t)v * D, X + (size_t)x * D, D, metric), x, false});
+      }
+    }
+    std::unordered_set<uint32_t> taken;
+    uint32_t* out = graph + (size_t)v * R;
+    float* outd = edge_dist + (size_t)v * R;
+    // prefix: slot by slot
+    for (int s = 0; s < P; ++s) {
+      out[s] = row[s];
+      outd[s] = rowd[s];
+      if (row[s] == SENT || !dead(tomb, row[s])) continue;
+      const uint32_t p = row[s];
+      const Entry* best = nullptr;
+      for (const Entry& e : U) {
+        if (taken.count(e.id)) continue;
+        bool from_p = false;
+        for (int t = 0; t < R && !from_p; ++t) from_p = snap[(size_t)p * R + t] == e.id;
+        if (from_p && (!best || key_less(e, *best))) best = &e;
+      }
+      if (best) {
+        out[s] = best->id;
+        outd[s] = best->d;
+        taken.insert(best->id);
+      } else {
+        out[s] = SENT;
+        outd[s] = INF;
+      }
+    }
+    // tail: kept live entries + the m nearest untaken members of U, sorted by key
+    std::vector<Entry> tail;
+    int m = 0;
+    for (int s = P; s < R; ++s) {
+      if (row[s] != SENT && !dead(tomb, row[s])) tail.push_back({rowd[s], row[s], false});
+      else m++;
+    }
+    std::vector<Entry> rest;
+    for (const Entry& e : U)
+      if (!taken.count(e.id)) rest.push_back(e);
+    std::sort(rest.begin(), rest.end(), key_less);
+    for (int i = 0; i < m && i < (int)rest.size(); ++i) tail.push_back(rest[i]);
+    std::sort(tail.begin(), tail.end(), key_less);
+    for (int s = P; s < R; ++s) {
+      const int i = s - P;
+      out[s] = i < (int)tail.size() ? tail[i].id : SENT;
+      outd[s] = i < (int)tail.size() ? tail[i].d : INF;
+    }
+    rewritten++;
+  }
+  *n_rewritten = rewritten;
+  return 0;
+}
+
 // O6: merge of per-shard top-k lists (global ids) into the first k by key.
 int orc_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids, float* out_d) {
   for (int64_t q = 0; q < nq; ++q) {

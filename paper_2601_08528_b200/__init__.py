@@ -18,7 +18,7 @@ try:  # torch is plumbing only (device memory, streams, process groups)
 except Exception:  # pragma: no cover
     torch = None
 
-__all__ = ["Index", "merge_topk", "SvfError", "SENTINEL", "default_params"]
+__all__ = ["Index", "merge_topk", "shard_premerge", "merge_pairs", "SvfError", "SENTINEL", "default_params"]
 
 
 def _is_torch(x) -> bool:
@@ -194,6 +194,13 @@ class Index:
         check(lib().svf_knn_exact(self._h, qp, nq, k, ip, dp, _stream(dev)))
         return ids, d
 
+    def knn_exact_into(self, Q, k: int, out_ids, out_dists):
+        """svf_knn_exact into caller-owned CUDA tensors."""
+        qp, qk, dev = _prep(Q, np.float32, torch.float32 if torch else None)
+        check(lib().svf_knn_exact(self._h, qp, int(qk.shape[0]), k, out_ids.data_ptr(), out_dists.data_ptr(),
+                                  _stream(dev)))
+        return out_ids, out_dists
+
     def link_candidates(self, cand_ids, cand_d, X=None):
         """TEST ENTRY (svf_link_candidates): steps (ii)+(iii) of insertion from given candidate lists."""
         ci = np.ascontiguousarray(cand_ids, dtype=np.uint32)
@@ -294,4 +301,26 @@ def merge_topk(ids, dists):
     od = torch.empty((nq, k), dtype=torch.float32, device=ids.device)
     check(lib().svf_merge_topk(ids.data_ptr(), dists.data_ptr(), G, nq, kk, oi.data_ptr(), od.data_ptr(),
                                _stream(ids.device)))
+    return oi, od
+
+
+def shard_premerge(ids, dists, n_logical: int, shards):
+    """K-M pre-merge of a rank's shard results (svf_shard_premerge): ids/dists [n, nq, k] CUDA
+    tensors of LOCAL ids from shards `shards` -> [nq, k] int64 packed pairs (dist bits << 32 | global id)."""
+    n, nq, k = ids.shape
+    sh = (ctypes.c_uint32 * n)(*[int(s) for s in shards])
+    out = torch.empty((nq, k), dtype=torch.int64, device=ids.device)
+    check(lib().svf_shard_premerge(ids.data_ptr(), dists.data_ptr(), n, nq, k, n_logical, sh, out.data_ptr(),
+                                   _stream(ids.device)))
+    return out
+
+
+def merge_pairs(pairs):
+    """K-M merge of G all-gathered pair lists (svf_merge_pairs): [G, nq, k] int64 CUDA tensor
+    -> (ids int32 [nq, k], dists f32 [nq, k]), the first k by (dist, id)."""
+    G, nq, k = pairs.shape
+    pairs = pairs.contiguous()
+    oi = torch.empty((nq, k), dtype=torch.int32, device=pairs.device)
+    od = torch.empty((nq, k), dtype=torch.float32, device=pairs.device)
+    check(lib().svf_merge_pairs(pairs.data_ptr(), G, nq, k, oi.data_ptr(), od.data_ptr(), _stream(pairs.device)))
     return oi, od

@@ -14,7 +14,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "CAPACITY", 3: "NOT_FOUND", 4: "CUDA",
 SENTINEL = 0xFFFFFFFF
 
 EXPORTED = ["svf_default_params", "svf_build", "svf_search", "svf_insert", "svf_delete", "svf_knn_exact",
-            "svf_merge_topk", "svf_export", "svf_import", "svf_link_candidates", "svf_set_search_params",
+            "svf_merge_topk", "svf_shard_premerge", "svf_merge_pairs", "svf_export", "svf_import", "svf_link_candidates", "svf_set_search_params",
             "svf_last_search_counters", "svf_set_knn_mode", "svf_knn_stats", "svf_set_warps_per_query", "svf_set_search_handoff", "svf_set_trace", "svf_read_trace", "svf_repair", "svf_consolidate", "svf_set_consolidation", "svf_consolidation_stats", "svf_profile", "svf_profile_read", "svf_info", "svf_destroy",
             "svf_last_error"]
 
@@ -56,6 +56,8 @@ def lib() -> ctypes.CDLL:
         "svf_delete": (ctypes.c_int, [P, P, I64, ctypes.POINTER(I64), P]),
         "svf_knn_exact": (ctypes.c_int, [P, P, I64, I32, P, P, P]),
         "svf_merge_topk": (ctypes.c_int, [P, P, I32, I64, I32, P, P, P]),
+        "svf_shard_premerge": (ctypes.c_int, [P, P, I32, I64, I32, ctypes.c_uint32, P, P, P]),
+        "svf_merge_pairs": (ctypes.c_int, [P, I32, I64, I32, P, P, P]),
         "svf_export": (ctypes.c_int, [P, P, P, P, P, ctypes.POINTER(I64)]),
         "svf_import": (ctypes.c_int, [ctypes.POINTER(SvfParams), P, P, P, P, I64, PP]),
         "svf_link_candidates": (ctypes.c_int, [P, P, P, P, I64, I32, P]),

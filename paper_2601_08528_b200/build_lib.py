@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsvf.so")
 SOURCES = ["index.cu", "search.cu", "search_d0.cu", "search_d24.cu", "search_d32.cu", "search_d50.cu", "link.cu",
            "knn.cu", "knn_tc.cu", "repair.cu"]
-HEADERS = ["common.cuh", "kernels.h", "search_impl.cuh", os.path.join("..", "..", "include", "svf.h")]
+HEADERS = ["common.cuh", "kernels.h", "search_impl.cuh", "search_lp.cuh", os.path.join("..", "..", "include", "svf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("SVF_NVCC_EXTRA", "").split()
@@ -35,7 +35,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, extra: tup
     flags_same = os.path.exists(flagfile) and open(flagfile).read() == " ".join(FLAGS + list(extra))
     def hdr_t(src):  # search_impl.cuh is included by the search TUs only
         return max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS
-                   if src.startswith("search") or h != "search_impl.cuh")
+                   if src.startswith("search") or h not in ("search_impl.cuh", "search_lp.cuh"))
 
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))

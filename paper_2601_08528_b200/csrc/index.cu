@@ -15,7 +15,7 @@ using namespace svf;
 
 struct svf_index {
   svf_params p{};
-  int dev = 0, num_sms = 148;
+  int dev = 0, num_sms = 148, smem_optin = 227 * 1024;
   int D = 0, Dp = 0, dq = 0, R = 0, P = 0;
   int64_t cap = 0, n_alloc = 0, n_deleted = 0;
   float* vec = nullptr;
@@ -152,8 +152,25 @@ int pow2_at_least(int x) {
 }
 
 struct SearchCfg {
-  int kpl, cpl, hbits, team, nv, n_init, wpq;
+  int kpl, cpl, hbits, team, nv, n_init, wpq, lp;
 };
+
+// K-S-L (shared-memory pool kernel) for pools of more than 64 keys; SVF_LP=0 keeps the register-pool kernel (A/B)
+bool lp_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SVF_LP");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+// default K-S-L visited-cache size (2^bits direct-mapped slots); SVF_LP_BITS overrides it for tuning
+int lp_bits_auto(int L) {
+  static const int env = [] {
+    const char* v = getenv("SVF_LP_BITS");
+    return v ? atoi(v) : 0;
+  }();
+  return env > 0 ? env : (L <= 256 ? 11 : 12);
+}
 
 bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, SearchCfg& c, std::string& why) {
   if (p < 1 || p > 8) return why = "search_width must be in [1, 8]", false;
@@ -173,8 +190,20 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   // 4096 slots for 128 < L <= 256 (C4 2M x 200, L_build 512: itopk 192 27.5 -> 15.4 ms, 256 37.6 -> 19.7 ms vs
   // 8192 slots, identical results; 2048 slots is 2% faster again but recomputes 1.6x; profiles/c4_2m_hash.json)
   const int autobits = L <= 16 ? 10 : (L <= 128 ? 11 : (L <= 256 ? 12 : 13));
-  c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
+  // K-S-L for pools of more than 64 keys (one warp per query): its direct-mapped visited cache needs no load
+  // invariant, only room to stage the query row
+  c.lp = LP > 64 && idx->wpq != 2 && lp_enabled();
+  if (c.lp) {
+    int lpmin = 8;
+    while ((1 << lpmin) < idx->Dp) ++lpmin;
+    c.hbits = std::max(hash_bits > 0 ? hash_bits : lp_bits_auto(L), lpmin);
+  } else {
+    c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
+  }
   if (c.hbits > 15) return why = "hash_bits too large", false;
+  // a configuration whose block does not fit the opt-in shared memory is refused up front (INVALID, index intact)
+  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp) > (size_t)idx->smem_optin)
+    return why = "hash_bits too large: the search block's visited tables exceed the shared memory per block", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
   c.n_init = n_init > 0 ? n_init : L;
@@ -318,13 +347,14 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   // needs at most half of the resident warp slots (~24 per SM), else 1.
   a.wpq = c.wpq;
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
+  a.large_pool = c.lp && a.wpq == 1;
   cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   unsigned long long*& hob = update_path ? idx->ho_upd : idx->ho;
   // one-warp batches: stragglers are handed to a chained pair-mode grid once few warps are left (SearchArgs::ho)
   a.ho = nullptr;
   a.ho_thresh = a.wpq == 1 ? (idx->ho_pct >= 0 ? idx->ho_pct : handoff_auto()) : 0;
-  if (a.ho_thresh > 0 && c.kpl <= kHandoffMaxKpl && c.cpl >= 2) {
+  if (a.ho_thresh > 0 && c.kpl <= kHandoffMaxKpl && c.cpl >= 2 && !a.large_pool) {
     if (hob == nullptr) {
       e = cudaMalloc(&hob, handoff_words() * 8);
       if (e != cudaSuccess) return e;
@@ -397,6 +427,7 @@ svf_status alloc_index(const svf_params* p, svf_index** out) {
   idx->p = *p;
   idx->dev = p->device;
   cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  cudaDeviceGetAttribute(&idx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
   idx->D = p->dim;
   idx->Dp = (p->dim + 3) / 4 * 4;
   idx->dq = idx->Dp / 4;
@@ -755,6 +786,36 @@ svf_status svf_merge_topk(const uint32_t* ids, const float* dists, int32_t G, in
   return SVF_OK;
 }
 
+svf_status svf_shard_premerge(const uint32_t* ids, const float* dists, int32_t n_lists, int64_t nq, int32_t k,
+                              uint32_t n_logical, const uint32_t* shard, uint64_t* out_pairs, void* stream) {
+  if (n_lists < 1 || n_lists > 16 || nq < 0 || k < 1 || k > 256 || n_logical < 1)
+    return fail(SVF_ERR_INVALID, "need 1 <= n_lists <= 16, nq >= 0, 1 <= k <= 256, n_logical >= 1");
+  if (nq == 0) return SVF_OK;
+  if (!ids || !dists || !shard || !out_pairs) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (!is_device_ptr(ids) || !is_device_ptr(dists) || !is_device_ptr(out_pairs))
+    return fail(SVF_ERR_INVALID, "svf_shard_premerge takes device ids/dists/out_pairs");
+  for (int i = 0; i < n_lists; ++i)
+    if (shard[i] >= n_logical) return fail(SVF_ERR_INVALID, "shard index >= n_logical");
+  cudaError_t e = launch_shard_premerge(ids, dists, n_lists, nq, k, n_logical, shard,
+                                        reinterpret_cast<unsigned long long*>(out_pairs),
+                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "shard pre-merge kernel");
+  return SVF_OK;
+}
+
+svf_status svf_merge_pairs(const uint64_t* pairs, int32_t G, int64_t nq, int32_t k, uint32_t* out_ids,
+                           float* out_dists, void* stream) {
+  if (G < 1 || nq < 0 || k < 1 || k > 256) return fail(SVF_ERR_INVALID, "need G >= 1, nq >= 0, 1 <= k <= 256");
+  if (nq == 0) return SVF_OK;
+  if (!pairs || !out_ids || !out_dists) return fail(SVF_ERR_INVALID, "NULL argument");
+  if (!is_device_ptr(pairs) || !is_device_ptr(out_ids) || !is_device_ptr(out_dists))
+    return fail(SVF_ERR_INVALID, "svf_merge_pairs takes device pointers (the all-gather output)");
+  cudaError_t e = launch_merge_pairs(reinterpret_cast<const unsigned long long*>(pairs), G, nq, k, out_ids,
+                                     out_dists, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "pair merge kernel");
+  return SVF_OK;
+}
+
 svf_status svf_export(const svf_index* cidx, float* vec, uint32_t* graph, float* edge_dist, uint32_t* tomb,
                       int64_t* n_alloc) {
   svf_index* idx = const_cast<svf_index*>(cidx);
@@ -809,6 +870,7 @@ svf_status svf_link_candidates(svf_index* idx, const float* X, const uint32_t* c
      launch_reverse(idx->graph, idx->edge_dist, idx->n_deleted > 0 ? idx->tomb : nullptr, idx->R, idx->P, first,
                     n_new, sp + 2 * cb, idx->scratch_bytes - 2 * cb, st),
      "reverse edges");
+  CK(idx, launch_store_u64(idx->small + 6, (uint64_t)(first + n_new), st), "publish n_visible");
   CK(idx, cudaStreamSynchronize(st), "link sync");
   idx->n_alloc += n_new;
   return SVF_OK;
@@ -908,11 +970,22 @@ svf_status svf_repair(svf_index* idx, int32_t c, double threshold, int64_t* n_re
   return repair_impl(idx, c, threshold, n_repaired, hist, static_cast<cudaStream_t>(stream));
 }
 
-// NEXT-4 global consolidation: every live vertex with a deleted neighbour p gets all live members of
-// N_out(p) as candidates (repair with c = R and threshold 0, reading C1 in DESIGN.md)
+// NEXT-4 global consolidation, reading C2: every live row holding a tombstoned id keeps its
+// live entries and refills its vacancies from the live members of its deleted neighbours' lists
 static svf_status consolidate_impl(svf_index* idx, int64_t* n_rewritten, cudaStream_t st) {
-  svf_status s = repair_impl(idx, idx->R, 0.0, n_rewritten, nullptr, st);
-  if (s != SVF_OK) return s;
+  int64_t n_list = 0;
+  if (idx->n_deleted > 0) {
+    CK(idx, ensure_scratch(idx, repair_mark_scratch_bytes(idx->n_alloc), st), "consolidation scratch");
+    uint64_t h[5];
+    CK(idx, launch_repair_mark(idx->graph, idx->tomb, idx->R, idx->n_alloc, 0.0, idx->scratch, st, &n_list, h),
+       "consolidation mark");
+    CK(idx,
+       launch_consolidate(idx->graph, idx->edge_dist, idx->vec, idx->dq, idx->p.metric, idx->tomb, idx->R, idx->P,
+                          idx->scratch, n_list, idx->num_sms, st),
+       "consolidation");
+    CK(idx, cudaStreamSynchronize(st), "consolidation sync");
+  }
+  if (n_rewritten) *n_rewritten = n_list;
   idx->deleted_at_consolidation = idx->n_deleted;
   idx->consolidations++;
   return SVF_OK;

@@ -74,8 +74,11 @@ struct SearchArgs {
   const unsigned int* q_flags;
   unsigned int q_epoch;
   int q_chunk_log2;
+  int large_pool;          // 1: K-S-L, the shared-memory pool kernel (search_lp.cuh; one warp per query, no handoff)
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
+// dynamic shared memory of one search block for a configuration (search_d0.cu); large_pool: K-S-L's layout
+size_t search_smem_bytes(int hbits, int kpl, int cpl, int L, int large_pool);
 
 // K-L1: detour-ranked forward rows for new ids [first, first + n_new) from candidates [n_new][nc]
 // (reads the snapshot rows of the candidates, writes rows first..first+n_new-1; disjoint by construction)
@@ -115,6 +118,13 @@ cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* t
 // K-M: merge G lists [G][nq][k] (ids/dists) -> first k per query by (dist, id)
 cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
                               float* out_d, cudaStream_t st);
+// K-M variants of the sharded search: a rank's pre-merge of its shards' LOCAL-id lists into packed
+// (distance bits << 32 | global id) pairs, g = local * n_logical + shard[i]; and the merge of the all-gathered pairs
+cudaError_t launch_shard_premerge(const uint32_t* ids, const float* d, int n_lists, int64_t nq, int k,
+                                  uint32_t n_logical, const uint32_t* shard, unsigned long long* out_pairs,
+                                  cudaStream_t st);
+cudaError_t launch_merge_pairs(const unsigned long long* pairs, int G, int64_t nq, int k, uint32_t* out_ids,
+                               float* out_d, cudaStream_t st);
 
 // NEXT-1 localized repair (repair.cu)
 // phase 1: V^L list + histogram (returns |V^L| after a sync); phase 2: rewrite those rows (reading R1')
@@ -125,6 +135,12 @@ size_t repair_apply_scratch_bytes(int64_t n_list, int R, int cap);
 cudaError_t launch_repair_apply(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
                                 const uint32_t* tomb, int R, int P, int c, int cap, const void* mark_scratch,
                                 int64_t n_list, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t st);
+
+// NEXT-4 global consolidation (reading C2): rewrite, in place, every row of the mark list (threshold 0 = every live
+// row holding a tombstoned id)
+cudaError_t launch_consolidate(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                               const uint32_t* tomb, int R, int P, const void* mark_scratch, int64_t n_list, int num_sms,
+                               cudaStream_t st);
 
 // small helpers
 cudaError_t launch_pad_rows(const float* src, int64_t n, int dim, float* dst, int dq, cudaStream_t st);

@@ -151,10 +151,17 @@ __global__ void merge_keys_kernel(const uint64_t* __restrict__ part, int S, int6
   }
 }
 
-// K-M: lists of (ids, dists) [G][nq][k] -> first k per query (inputs need not be sorted)
-template <int KPL>
-__global__ void merge_topk_kernel(const uint32_t* __restrict__ ids, const float* __restrict__ d, int G, int64_t nq,
-                                  int k, uint32_t* __restrict__ out_ids, float* __restrict__ out_d) {
+// K-M: lists [G][nq][k] -> first k per query by (dist, id) (inputs need not be sorted).  Input entries are either
+// separate (ids, d) arrays or packed pairs (distance bits << 32 | id); list g's ids may be mapped to global ids
+// id * id_mul + add.v[g] (a rank's shards); the output is separate arrays or packed pairs.
+struct IdAdd {
+  uint32_t v[16];
+};
+template <int KPL, bool IN_PAIRS, bool OUT_PAIRS>
+__global__ void merge_topk_kernel(const uint32_t* __restrict__ ids, const float* __restrict__ d,
+                                  const unsigned long long* __restrict__ pairs, int G, int64_t nq, int k,
+                                  uint32_t id_mul, IdAdd add, uint32_t* __restrict__ out_ids,
+                                  float* __restrict__ out_d, unsigned long long* __restrict__ out_pairs) {
   const int lane = threadIdx.x & 31;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (qi >= nq) return;
@@ -169,8 +176,17 @@ __global__ void merge_topk_kernel(const uint32_t* __restrict__ ids, const float*
       const int e = r * 32 + lane;
       c[r] = kEmptyKey;
       if (e < k) {
-        const uint32_t id = ids[o + e];
-        if (id != kSent) c[r] = make_key(d[o + e] + 0.0f, id);
+        uint32_t id;
+        float dist;
+        if (IN_PAIRS) {
+          const unsigned long long pr = pairs[o + e];
+          id = (uint32_t)pr;
+          dist = __uint_as_float((uint32_t)(pr >> 32));
+        } else {
+          id = ids[o + e];
+          dist = d[o + e];
+        }
+        if (id != kSent) c[r] = make_key(dist + 0.0f, id_mul ? id * id_mul + add.v[g] : id);
       }
     }
     warp_sort<KPL>(c, lane);
@@ -180,8 +196,13 @@ __global__ void merge_topk_kernel(const uint32_t* __restrict__ ids, const float*
   for (int r = 0; r < KPL; ++r) {
     const int e = r * 32 + lane;
     if (e < k) {
-      out_ids[qi * k + e] = key_id(best[r]);
-      out_d[qi * k + e] = key_dist(best[r]);
+      if (OUT_PAIRS) {
+        out_pairs[qi * k + e] =
+            ((unsigned long long)__float_as_uint(key_dist(best[r])) << 32) | (unsigned long long)key_id(best[r]);
+      } else {
+        out_ids[qi * k + e] = key_id(best[r]);
+        out_d[qi * k + e] = key_dist(best[r]);
+      }
     }
   }
 }
@@ -253,18 +274,39 @@ cudaError_t launch_knn_exact(const float* vec, int dq, int64_t n, const uint32_t
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
-                              float* out_d, cudaStream_t st) {
+template <bool IN_PAIRS, bool OUT_PAIRS>
+static cudaError_t merge_launch(const uint32_t* ids, const float* d, const unsigned long long* pairs, int G, int64_t nq,
+                                int k, uint32_t id_mul, const IdAdd& add, uint32_t* out_ids, float* out_d,
+                                unsigned long long* out_pairs, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((nq + 7) / 8);
   switch (kpl_for(k)) {
-    case 1: merge_topk_kernel<1><<<blocks, 256, 0, st>>>(ids, d, G, nq, k, out_ids, out_d); break;
-    case 2: merge_topk_kernel<2><<<blocks, 256, 0, st>>>(ids, d, G, nq, k, out_ids, out_d); break;
-    case 4: merge_topk_kernel<4><<<blocks, 256, 0, st>>>(ids, d, G, nq, k, out_ids, out_d); break;
-    case 8: merge_topk_kernel<8><<<blocks, 256, 0, st>>>(ids, d, G, nq, k, out_ids, out_d); break;
+    case 1: merge_topk_kernel<1, IN_PAIRS, OUT_PAIRS><<<blocks, 256, 0, st>>>(ids, d, pairs, G, nq, k, id_mul, add, out_ids, out_d, out_pairs); break;
+    case 2: merge_topk_kernel<2, IN_PAIRS, OUT_PAIRS><<<blocks, 256, 0, st>>>(ids, d, pairs, G, nq, k, id_mul, add, out_ids, out_d, out_pairs); break;
+    case 4: merge_topk_kernel<4, IN_PAIRS, OUT_PAIRS><<<blocks, 256, 0, st>>>(ids, d, pairs, G, nq, k, id_mul, add, out_ids, out_d, out_pairs); break;
+    case 8: merge_topk_kernel<8, IN_PAIRS, OUT_PAIRS><<<blocks, 256, 0, st>>>(ids, d, pairs, G, nq, k, id_mul, add, out_ids, out_d, out_pairs); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,
+                              float* out_d, cudaStream_t st) {
+  return merge_launch<false, false>(ids, d, nullptr, G, nq, k, 0, IdAdd{}, out_ids, out_d, nullptr, st);
+}
+
+cudaError_t launch_shard_premerge(const uint32_t* ids, const float* d, int n_lists, int64_t nq, int k,
+                                  uint32_t n_logical, const uint32_t* shard, unsigned long long* out_pairs,
+                                  cudaStream_t st) {
+  if (n_lists < 1 || n_lists > 16) return cudaErrorInvalidValue;
+  IdAdd add{};
+  for (int i = 0; i < n_lists; ++i) add.v[i] = shard[i];
+  return merge_launch<false, true>(ids, d, nullptr, n_lists, nq, k, n_logical, add, nullptr, nullptr, out_pairs, st);
+}
+
+cudaError_t launch_merge_pairs(const unsigned long long* pairs, int G, int64_t nq, int k, uint32_t* out_ids,
+                               float* out_d, cudaStream_t st) {
+  return merge_launch<true, false>(nullptr, nullptr, pairs, G, nq, k, 0, IdAdd{}, out_ids, out_d, nullptr, st);
 }
 
 }  // namespace svf

@@ -173,6 +173,206 @@ __global__ void __launch_bounds__(kRepWarps * 32)
   }
 }
 
+// insert-if-absent: true when id was not in the set (concurrent inserts of one id: exactly one lane wins)
+__device__ __forceinline__ bool set_add(uint32_t* tab, int bits, uint32_t id) {
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t h = (id * 0x9E3779B1u) >> (32 - bits);
+  for (;;) {
+    const uint32_t prev = atomicCAS(tab + h, kSent, id);
+    if (prev == kSent) return true;
+    if (prev == id) return false;
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ float row_dist(const float4* __restrict__ xv, const float4* __restrict__ xc, int dq,
+                                          int metric) {
+  float acc = 0.f;
+  for (int j = 0; j < dq; ++j) {
+    const float4 a = __ldg(xv + j), b = __ldg(xc + j);
+    if (metric == 0) {
+      const float d0 = b.x - a.x, d1 = b.y - a.y, d2 = b.z - a.z, d3 = b.w - a.w;
+      acc = fmaf(d0, d0, acc);
+      acc = fmaf(d1, d1, acc);
+      acc = fmaf(d2, d2, acc);
+      acc = fmaf(d3, d3, acc);
+    } else {
+      acc = fmaf(b.x, a.x, acc);
+      acc = fmaf(b.y, a.y, acc);
+      acc = fmaf(b.z, a.z, acc);
+      acc = fmaf(b.w, a.w, acc);
+    }
+  }
+  return (metric == 0 ? acc : -acc) + 0.0f;  // canonical +0
+}
+
+// NEXT-4 global consolidation, reading C2 (oracle orc_consolidate), warp per affected live vertex v (a
+// row holding a tombstoned id).  Only tombstoned rows N_out(p) are read besides v's own row, and those are frozen,
+// so every warp rewrites its row in place:
+//   prefix: each tombstoned slot s < P (slot order) <- the nearest (dist, id) live member of N_out(p_s) that is not
+//           v, not a live entry of row(v) and not taken by an earlier slot (empty when none);
+//   tail:   the live tail entries stay; the m vacancies take the m nearest remaining members of the union of the
+//           deleted neighbours' lists (deduplicated), streamed in chunks of <= buf_cap ids into a running top list;
+//           the tail is re-sorted by key, empty slots last.
+// tab holds row(v)'s live ids, the prefix refills and every union member seen (one set: all three are excluded).
+template <int ER, int EU>
+__global__ void __launch_bounds__(kRepWarps * 32)
+    consolidate_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist, const float* __restrict__ vec,
+                       int dq, int metric, const uint32_t* __restrict__ tomb, int R, int P,
+                       const uint32_t* __restrict__ list, int64_t n_list, int set_bits, int buf_cap) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)buf_cap * 4 + (size_t)buf_cap * 8 + 15) & ~(size_t)15;
+  unsigned char* base = smem + per_warp * wib;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(base);
+  uint32_t* cid = tab + (1 << set_bits);
+  uint64_t* ckey = reinterpret_cast<uint64_t*>(cid + buf_cap);
+  const int wpb = blockDim.x >> 5;
+  const float4* v4 = reinterpret_cast<const float4*>(vec);
+  for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < n_list; w += (int64_t)gridDim.x * wpb) {
+    const uint32_t v = list[w];
+    for (int i = lane; i < (1 << set_bits); i += 32) tab[i] = kSent;
+    __syncwarp();
+    uint32_t rid[ER], orig[ER];
+    float rd[ER];
+    bool dead_slot[ER];
+    // slot s of a register-striped row (element s = r*32 + lane), without dynamic register indexing
+    auto slot_of = [&](const uint32_t (&a)[ER], int s) {
+      uint32_t x = kSent;
+#pragma unroll
+      for (int r = 0; r < ER; ++r) {
+        const uint32_t y = __shfl_sync(0xffffffffu, a[r], s & 31);
+        if (r == (s >> 5)) x = y;
+      }
+      return x;
+    };
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      rid[r] = s < R ? graph[(size_t)v * R + s] : kSent;
+      orig[r] = rid[r];
+      rd[r] = s < R ? edge_dist[(size_t)v * R + s] : 0.f;
+      dead_slot[r] = rid[r] != kSent && tomb_dead(tomb, rid[r]);
+      if (rid[r] != kSent && !dead_slot[r]) set_add(tab, set_bits, rid[r]);
+    }
+    __syncwarp();
+    const float4* xv = v4 + (size_t)v * dq;
+    // prefix slots in slot order
+    for (int s = 0; s < P; ++s) {
+      const uint32_t p = slot_of(orig, s);
+      if (p == kSent || !tomb_dead(tomb, p)) continue;
+      uint64_t bk = kEmptyKey;
+#pragma unroll
+      for (int r2 = 0; r2 < ER; ++r2) {
+        const int t = r2 * 32 + lane;
+        const uint32_t x = t < R ? graph[(size_t)p * R + t] : kSent;
+        if (x != kSent && x != v && !tomb_dead(tomb, x) && !set_has(tab, set_bits, x)) {
+          const uint64_t kk = make_key(row_dist(xv, v4 + (size_t)x * dq, dq, metric), x);
+          bk = kk < bk ? kk : bk;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, bk, off);
+        bk = o < bk ? o : bk;
+      }
+      __syncwarp();
+      if (lane == 0 && bk != kEmptyKey) set_add(tab, set_bits, key_id(bk));
+#pragma unroll
+      for (int r = 0; r < ER; ++r)
+        if (r == (s >> 5) && (s & 31) == lane) {  // the owning lane updates its register copy of the row
+          rid[r] = key_id(bk);
+          rd[r] = key_dist(bk);
+        }
+      __syncwarp();
+    }
+    // tail: m vacancies, refilled from the union of the deleted neighbours' lists
+    int m = 0;
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      m += __popc(__ballot_sync(0xffffffffu, s >= P && s < R && (rid[r] == kSent || dead_slot[r])));
+    }
+    uint64_t best[EU];
+#pragma unroll
+    for (int r = 0; r < EU; ++r) best[r] = kEmptyKey;
+    int ncand = 0;
+    auto flush = [&]() {
+      for (int i = lane; i < ncand; i += 32) ckey[i] = make_key(row_dist(xv, v4 + (size_t)cid[i] * dq, dq, metric), cid[i]);
+      __syncwarp();
+      for (int c0 = 0; c0 < ncand; c0 += 32) {
+        uint64_t cc[1];
+        cc[0] = c0 + lane < ncand ? ckey[c0 + lane] : kEmptyKey;
+        warp_sort<1>(cc, lane);
+        warp_merge_into<EU, 1>(best, cc, lane);
+      }
+      __syncwarp();
+      ncand = 0;
+    };
+    if (m > 0) {
+      for (int s = 0; s < R; ++s) {
+        // the original row's deleted entries (the prefix registers now hold the refills)
+        const uint32_t p = slot_of(orig, s);
+        if (p == kSent || !tomb_dead(tomb, p)) continue;
+        if (ncand + R > buf_cap) flush();
+#pragma unroll
+        for (int r2 = 0; r2 < ER; ++r2) {
+          const int t = r2 * 32 + lane;
+          const uint32_t x = t < R ? graph[(size_t)p * R + t] : kSent;
+          const bool ok = x != kSent && x != v && !tomb_dead(tomb, x) && set_add(tab, set_bits, x);
+          const unsigned mk = __ballot_sync(0xffffffffu, ok);
+          if (ok) cid[ncand + __popc(mk & ((1u << lane) - 1u))] = x;
+          ncand += __popc(mk);
+        }
+        __syncwarp();
+      }
+      flush();
+    }
+    // new tail = kept live tail entries U the first m of best, sorted by key
+    __syncwarp();
+    int nk = 0;
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      const bool keep = s >= P && s < R && rid[r] != kSent && !dead_slot[r];
+      const unsigned mk = __ballot_sync(0xffffffffu, keep);
+      if (keep) ckey[nk + __popc(mk & ((1u << lane) - 1u))] = make_key(rd[r], rid[r]);
+      nk += __popc(mk);
+    }
+#pragma unroll
+    for (int r = 0; r < EU; ++r) {
+      const int e = r * 32 + lane;
+      if (e < m) ckey[nk + e] = best[r];
+    }
+    __syncwarp();
+    uint64_t tl[EU];
+#pragma unroll
+    for (int r = 0; r < EU; ++r) {
+      const int e = r * 32 + lane;
+      tl[r] = e < nk + m ? ckey[e] : kEmptyKey;
+    }
+    warp_sort<EU>(tl, lane);
+    // the whole read of the starting row is done: write prefix (registers) and tail
+#pragma unroll
+    for (int r = 0; r < ER; ++r) {
+      const int s = r * 32 + lane;
+      if (s < P) {
+        graph[(size_t)v * R + s] = rid[r];
+        edge_dist[(size_t)v * R + s] = rid[r] == kSent ? __int_as_float(0x7F800000) : rd[r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < EU; ++r) {
+      const int e = r * 32 + lane;
+      if (P + e < R) {
+        graph[(size_t)v * R + P + e] = key_id(tl[r]);
+        edge_dist[(size_t)v * R + P + e] = key_dist(tl[r]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void repair_scatter_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist,
                                       const uint32_t* __restrict__ list, int64_t n_list, int R,
                                       const uint32_t* __restrict__ rows, const float* __restrict__ rows_d) {
@@ -255,6 +455,35 @@ cudaError_t launch_repair_apply(uint32_t* graph, float* edge_dist, const float* 
   repair_scatter_kernel<<<(unsigned)((n_list * R + 255) / 256), 256, 0, st>>>(graph, edge_dist, list, n_list, R, rows,
                                                                              rows_d);
   return cudaGetLastError();
+}
+
+cudaError_t launch_consolidate(uint32_t* graph, float* edge_dist, const float* vec, int dq, int metric,
+                               const uint32_t* tomb, int R, int P, const void* mark_scratch, int64_t n_list, int num_sms,
+                               cudaStream_t st) {
+  if (n_list <= 0) return cudaSuccess;
+  const uint32_t* list = static_cast<const uint32_t*>(mark_scratch);
+  // one set for the row, the prefix refills and the union (<= R + R*R ids): load <= 1/2 up to 2^13 slots, else 0.8
+  const int total = R + R * R;
+  int set_bits = 1;
+  while ((1 << set_bits) < 2 * total && set_bits < 13) ++set_bits;
+  while ((1 << set_bits) < total * 5 / 4) ++set_bits;
+  const int buf_cap = 2 * R;
+  const size_t per_warp = (((size_t)4 << set_bits) + (size_t)buf_cap * 12 + 15) & ~(size_t)15;
+  const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kRepWarps, (200u << 10) / per_warp));
+  const size_t smem = per_warp * wpb;
+  auto run = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<(unsigned)(num_sms * 8), wpb * 32, smem, st>>>(graph, edge_dist, vec, dq, metric, tomb, R, P, list,
+                                                                n_list, set_bits, buf_cap);
+    return cudaGetLastError();
+  };
+  const int T = R - P;  // tail slots
+  const int ER = R <= 32 ? 1 : R <= 64 ? 2 : 4;
+  const int EU = T <= 32 ? 1 : T <= 64 ? 2 : 4;
+  if (ER == 1) return run(consolidate_kernel<1, 1>);
+  if (ER == 2) return EU == 1 ? run(consolidate_kernel<2, 1>) : run(consolidate_kernel<2, 2>);
+  return EU == 1 ? run(consolidate_kernel<4, 1>) : EU == 2 ? run(consolidate_kernel<4, 2>) : run(consolidate_kernel<4, 4>);
 }
 
 }  // namespace svf

@@ -91,12 +91,11 @@ constexpr int gather_u() {
                   : (KPL >= 4 && DQT > 0) ? (Geo<DQT>::NV <= 3 ? 4 : 3) : SVF_GATHER_U;
 }
 
-// Distances of this warp's S survivors sid[0..S) -> keys; keep those strictly better than the pool's current L-th
-// key (the only ones that can enter: the pool keeps the L smallest of pool U cand), compacted into skey[0..S2).
-template <int KPL, int CPL, int DQT, int U>
-__device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
-                                         uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
-  // U = vectors per team per round (U * 32/T vectors in flight per warp)
+// Distances of the S ids sid[0..S) -> keys skey[0..S): teams of T lanes per vector, U vectors per team per round
+// (U * 32/T rows in flight per warp), coalesced 16-byte gathers, FFMA, xor-shuffle reduction.
+template <int DQT, int U>
+__device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
+                                            const float4 (&qv)[4], int lane) {
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
@@ -163,6 +162,14 @@ __device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&p
     }
   }
   __syncwarp();
+}
+
+// Distances of this warp's S survivors sid[0..S) -> keys; keep those strictly better than the pool's current L-th
+// key (the only ones that can enter: the pool keeps the L smallest of pool U cand), compacted into skey[0..S2).
+template <int KPL, int CPL, int DQT, int U>
+__device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
+                                         uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
+  gather_keys<DQT, U>(a, sid, skey, S, qv, lane);
   uint64_t kreg = kEmptyKey;
 #pragma unroll
   for (int r = 0; r < KPL; ++r)
@@ -710,7 +717,11 @@ static cudaError_t launch_kpl(SearchArgs a, int cpl, int num_sms, cudaStream_t s
 }
 
 template <int DQT>
+cudaError_t launch_search_lp_dq(SearchArgs a, int cpl, int num_sms, cudaStream_t st);
+
+template <int DQT>
 cudaError_t launch_search_dq(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st) {
+  if (a.large_pool) return launch_search_lp_dq<DQT>(a, cpl, num_sms, st);  // K-S-L (search_lp.cuh)
   switch (kpl) {
     case 1: return launch_kpl<1, DQT>(a, cpl, num_sms, st);
     case 2: return launch_kpl<2, DQT>(a, cpl, num_sms, st);
@@ -722,3 +733,5 @@ cudaError_t launch_search_dq(SearchArgs a, int kpl, int cpl, int num_sms, cudaSt
 }
 
 }  // namespace svf
+
+#include "search_lp.cuh"

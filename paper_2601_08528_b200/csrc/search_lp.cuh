@@ -1,0 +1,409 @@
+// K-S-L: the search of SURVEY §8(a) S0-S8 (Algorithm 1) for LARGE candidate pools (L > 64: the insert
+// search at L_insert = 128, C4's itopk 192, build searches at L_build 256-512).  Included by search_impl.cuh.
+//
+// Why a second kernel (DESIGN.md §6 "K-S-L"): the register-resident pool of K-S costs 4-16 u64 per lane plus an
+// unrolled bitonic merge over L keys; at L >= 128 that is 113-128 registers (4 blocks/SM, ~14 warps), ~1360 warp
+// instructions per iteration and a 2^11-2^12-slot probing visited table that is cleared and re-filled every ~40
+// iterations (measured: 6.6 us per iteration, 1.83x recomputed distances at L = 128, profiles/r02_pool_probe.json).
+// Here one warp still serves one query, but:
+//  - the pool lives in shared memory as a sorted array of exactly L 64-bit keys (dist, id, parented flag; I6);
+//    new keys are merged in place: each new key finds its insertion point by binary search, each moved pool key its
+//    shift by binary search over the (few) new keys, and the moving suffix is rewritten back to front in 32-key
+//    chunks (a merge is a bijection, so no position is written before it is read);
+//  - parents are found from a cursor: every entry before it is parented, and a merge can only move the first
+//    unparented entry up to the first inserted key;
+//  - the visited set is a direct-mapped cache of ids (slot = hash(id), overwritten on collision, never cleared
+//    mid-query, no atomics).  It may forget ids but never reports an unvisited one: reading I7 applies as for the
+//    probing table (a forgotten non-pool id is rejected again by the L-th key, which never increases), and a
+//    forgotten id that is still IN the pool is caught by an exact membership test (binary search) of the few keys
+//    that pass the L-th-key threshold.  Results are therefore identical to the exact visited set (oracle O2);
+//  - no per-lane pool registers: the gather engine keeps its registers, for more resident warps.
+#pragma once
+
+namespace svf {
+
+namespace {
+
+// per-warp shared memory: [cache 2^hbits u32 | pool Lp u64 | survivor ids MP u32 | keys MP u64 | new keys MP u64 |
+// insertion points MP u32 | query slot 2 u64 | parents 8 u32]
+struct LpLayout {
+  int hbits, Lp, MP;
+  __host__ __device__ size_t pool_off() const { return (size_t)4 << hbits; }
+  __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
+  __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
+  __host__ __device__ size_t ck_off() const { return skey_off() + (size_t)MP * 8; }
+  __host__ __device__ size_t cb_off() const { return ck_off() + (size_t)MP * 8; }
+  __host__ __device__ size_t misc_off() const { return cb_off() + (size_t)MP * 4; }
+  __host__ __device__ size_t warp_bytes() const { return (misc_off() + 48 + 15) & ~(size_t)15; }
+};
+
+#ifndef SVF_MINB_LP
+#define SVF_MINB_LP 6
+#endif
+#ifndef SVF_GATHER_U_LP
+#define SVF_GATHER_U_LP 2
+#endif
+
+__device__ __forceinline__ uint32_t cache_slot(uint32_t id, int hbits) { return (id * 0x9E3779B1u) >> (32 - hbits); }
+
+// number of keys in sorted a[0..n) whose flag-stripped value is < k (k has its flag bit clear)
+__device__ __forceinline__ int lower_bound_key(const uint64_t* a, int n, uint64_t k) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((a[mid] & ~1ull) < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <int CPL, int DQT>
+__global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search_lp_kernel(SearchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int MP = 32 * CPL;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP};
+  unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
+  uint32_t* cache = reinterpret_cast<uint32_t*>(base);
+  uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());
+  uint32_t* sid = reinterpret_cast<uint32_t*>(base + lay.sid_off());
+  uint64_t* skey = reinterpret_cast<uint64_t*>(base + lay.skey_off());
+  uint64_t* ck = reinterpret_cast<uint64_t*>(base + lay.ck_off());
+  uint32_t* cb = reinterpret_cast<uint32_t*>(base + lay.cb_off());
+  unsigned long long* qslot = reinterpret_cast<unsigned long long*>(base + lay.misc_off());
+  uint32_t* spar = reinterpret_cast<uint32_t*>(base + lay.misc_off() + 16);
+  const int H = 1 << a.hbits;
+  const int T = DQT ? Geo<DQT>::T : a.team;
+  const int tl = lane & (T - 1);
+  const int L = a.L;
+  constexpr int U = DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U;
+
+  for (;;) {
+    if (lane == 0) {
+      const unsigned long long f = atomicAdd(a.work_counter, 1ull);
+      if (a.q_flags != nullptr && f < (unsigned long long)a.nq) {  // streamed host queries: wait for the chunk
+        const volatile unsigned int* fl = a.q_flags + (f >> a.q_chunk_log2);
+        while (*fl != a.q_epoch) __nanosleep(64);
+        __threadfence();
+      }
+      unsigned long long nsnap = a.n_alloc;
+      if (a.n_visible != nullptr)
+        nsnap = min(nsnap, *reinterpret_cast<const volatile unsigned long long*>(a.n_visible));
+      qslot[0] = f;
+      qslot[1] = nsnap;
+    }
+    __syncwarp();
+    const unsigned long long qf = qslot[0];
+    const uint32_t n = (uint32_t)qslot[1];
+    __syncwarp();
+    if (qf >= (unsigned long long)a.nq) break;
+    const unsigned long long qi = qf;
+    unsigned long long t_start = 0;
+    if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+
+    // S0: stage the query through the cache region (coalesced), keep this lane's fragment, clear the cache
+    const float* qg = a.Q + (size_t)qi * a.q_stride;
+    float* qstage = reinterpret_cast<float*>(cache);
+    for (int i = lane; i < a.dq * 4; i += 32) qstage[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
+    __syncwarp();
+    float4 qv[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = tl + T * v;
+      qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? reinterpret_cast<const float4*>(qstage)[c]
+                                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    for (int i = lane; i < H; i += 32) cache[i] = kHashEmpty;
+    __syncwarp();
+
+    int np = 0;  // entries in the pool (<= L)
+    int fu = 0;  // every entry before fu is parented
+    uint32_t n_dist = 0, iters = 0, n_exp = 0;
+
+    // S6 C.Update for the keys skey[0..S): drop those not better than the L-th key, sort, drop duplicates and keys
+    // already in the pool, merge the rest in place
+    auto update = [&](int S) {
+      const uint64_t kth = np < L ? kEmptyKey : (pool[L - 1] & ~1ull);
+      int S2 = 0;
+#pragma unroll
+      for (int r = 0; r < CPL; ++r) {
+        const int e = r * 32 + lane;
+        const uint64_t k = e < S ? skey[e] : kEmptyKey;
+        const bool pass = k < kth;
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) ck[S2 + __popc(m & ((1u << lane) - 1u))] = k;
+        S2 += __popc(m);
+      }
+      if (S2 == 0) return;
+      __syncwarp();
+      int m = 0;
+      auto dedup_compact = [&](auto& c) {  // c: sorted register array (element e = r*32 + lane)
+        constexpr int E = sizeof(c) / sizeof(c[0]);
+        uint64_t prev_last = kEmptyKey;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int e = r * 32 + lane;
+          uint64_t prev = __shfl_up_sync(0xffffffffu, c[r], 1);
+          if (lane == 0) prev = prev_last;
+          prev_last = __shfl_sync(0xffffffffu, c[r], 31);
+          int b = 0;
+          bool keep = e < S2 && !(e > 0 && prev == c[r]);  // equal keys: the same id offered twice (p > 1)
+          if (keep) {
+            b = lower_bound_key(pool, np, c[r]);
+            keep = !(b < np && (pool[b] & ~1ull) == c[r]);  // already in the pool (the cache forgot it)
+          }
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int j = m + __popc(km & ((1u << lane) - 1u));
+            skey[j] = c[r];
+            cb[j] = (uint32_t)b;
+          }
+          m += __popc(km);
+        }
+      };
+      if (S2 <= 32) {
+        uint64_t c[1];
+        c[0] = lane < S2 ? ck[lane] : kEmptyKey;
+        warp_sort<1>(c, lane);
+        dedup_compact(c);
+      } else {
+        uint64_t c[CPL];
+#pragma unroll
+        for (int r = 0; r < CPL; ++r) c[r] = r * 32 + lane < S2 ? ck[r * 32 + lane] : kEmptyKey;
+        warp_sort<CPL>(c, lane);
+        dedup_compact(c);
+      }
+      if (m == 0) return;
+      __syncwarp();
+      // pool keys at [b0, np) move up by the number of new keys below them, back-to-front in 32-key chunks
+      const int b0 = (int)cb[0];
+      if (np > b0) {
+        for (int s0 = b0 + ((np - b0 - 1) & ~31); s0 >= b0; s0 -= 32) {
+          const int i = s0 + lane;
+          uint64_t pk = 0;
+          int dst = L;
+          if (i < np) {
+            pk = pool[i];
+            dst = i + lower_bound_key(skey, m, pk & ~1ull);
+          }
+          __syncwarp();
+          if (dst < L) pool[dst] = pk;
+          __syncwarp();
+        }
+      }
+      for (int j = lane; j < m; j += 32) {
+        const int dst = j + (int)cb[j];
+        if (dst < L) pool[dst] = skey[j];
+      }
+      __syncwarp();
+      np = min(L, np + m);
+      fu = min(fu, b0);
+    };
+
+    // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
+    if (n > 0) {
+      uint64_t pa = 0, pb = 0;
+      if (lane == 0) perm_params(a.seed, a.qidx_base + qi, n, pa, pb);
+      pa = __shfl_sync(0xffffffffu, pa, 0);
+      pb = __shfl_sync(0xffffffffu, pb, 0);
+      uint32_t cur = (uint32_t)((pa * (uint64_t)lane + pb) % n);
+      const uint32_t step32 = (uint32_t)((pa * 32ull) % n);
+      int taken = 0;
+      for (uint64_t j0 = 0; j0 < n && taken < a.n_init; j0 += MP) {
+        int running = 0;
+#pragma unroll
+        for (int r = 0; r < CPL; ++r) {
+          const uint64_t j = j0 + (uint64_t)(r * 32 + lane);
+          const uint32_t id = cur;
+          cur += step32;
+          if (cur >= n) cur -= n;
+          bool ok = j < n;
+          if (ok) ok = !tomb_dead(a.tomb, id);
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          const int pos = running + __popc(m & ((1u << lane) - 1u));
+          const bool keep = ok && taken + pos < a.n_init;
+          if (keep) {
+            sid[pos] = id;
+            cache[cache_slot(id, a.hbits)] = id;
+          }
+          running += __popc(m);
+        }
+        const int kept = min(running, a.n_init - taken);
+        taken += kept;
+        gather_keys<DQT, U>(a, sid, skey, kept, qv, lane);
+        n_dist += kept;
+        update(kept);
+      }
+    }
+
+    // S2-S7: expand the first p unparented entries until every pool entry is parented (I3, I4)
+    uint32_t spec_id = kSent;  // parent whose row sits in spec_row (speculative next-row load)
+    uint32_t spec_row[CPL];
+    for (;;) {
+      if (a.max_iter > 0 && (int)iters == a.max_iter) break;
+      // S2 GetNearest: scan from the cursor, mark the first p unparented entries
+      int npar = 0, last = -1;
+      for (int s0 = fu; s0 < np && npar < a.p; s0 += 32) {
+        const int i = s0 + lane;
+        const uint64_t k = i < np ? pool[i] : kEmptyKey;
+        unsigned m = __ballot_sync(0xffffffffu, (k & 1ull) == 0ull);
+        while (m != 0u && npar < a.p) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1u;
+          if (lane == l) {
+            pool[i] = k | 1ull;
+            spar[npar] = key_id(k);
+          }
+          ++npar;
+          last = s0 + l;
+        }
+      }
+      if (npar == 0) break;
+      __syncwarp();
+      // the next unparented entry after the last parent: the likely next parent and the new cursor
+      int nxt = np;
+      for (int s0 = last + 1; s0 < np; s0 += 32) {
+        const int i = s0 + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i < np && (pool[i] & 1ull) == 0ull);
+        if (m) {
+          nxt = s0 + __ffs(m) - 1;
+          break;
+        }
+      }
+      fu = nxt;
+      ++iters;
+      n_exp += npar;
+      const int ncand = npar * a.R;
+      // S3: neighbour rows (from the speculative registers when the guess held), coalesced
+      uint32_t rowv[CPL];
+      const bool hit = npar == 1 && spar[0] == spec_id;
+#pragma unroll
+      for (int r = 0; r < CPL; ++r) {
+        const int e = r * 32 + lane;
+        rowv[r] = kSent;
+        if (hit) {
+          rowv[r] = spec_row[r];
+        } else if (e < ncand) {
+          const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
+          rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
+        }
+      }
+      spec_id = kSent;
+      if (nxt < np) {
+        const uint32_t nid = key_id(pool[nxt]);
+        if (a.p == 1) {
+          spec_id = nid;
+#pragma unroll
+          for (int r = 0; r < CPL; ++r) {
+            const int e = r * 32 + lane;
+            spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
+          }
+        } else if (lane < ((a.R * 4 + 127) >> 7)) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.graph + (size_t)nid * a.R + lane * 32));
+        }
+      }
+      // S4: sentinel / snapshot / tombstone / visited-cache filters
+      int running = 0;
+#pragma unroll
+      for (int r = 0; r < CPL; ++r) {
+        const uint32_t id = rowv[r];
+        bool ok = id != kSent && (uint64_t)id < n;
+        if (ok) ok = !tomb_dead(a.tomb, id);
+        uint32_t slot = 0;
+        if (ok) {
+          slot = cache_slot(id, a.hbits);
+          ok = cache[slot] != id;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+          sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+          cache[slot] = id;
+        }
+        running += __popc(m);
+      }
+      if (running == 0) continue;
+      // S5 distances, S6 merge
+      gather_keys<DQT, U>(a, sid, skey, running, qv, lane);
+      n_dist += running;
+      update(running);
+    }
+
+    // S8: emit the first n_out entries (k, or the whole pool in insert mode)
+    for (int e = lane; e < a.n_out; e += 32) {
+      const uint64_t k = e < np ? pool[e] : kEmptyKey;
+      a.out_ids[(size_t)qi * a.n_out + e] = key_id(k);
+      a.out_d[(size_t)qi * a.n_out + e] = key_dist(k);
+    }
+    if (lane == 0) {
+      if (a.counters != nullptr) {
+        a.counters[qi * 3 + 0] = n_dist;
+        a.counters[qi * 3 + 1] = iters;
+        a.counters[qi * 3 + 2] = n_exp;
+      }
+      if (a.trace != nullptr) {
+        unsigned long long t_end;
+        unsigned int smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* row = a.trace + qi * kTraceCols;
+        row[0] = t_start;
+        row[1] = t_end;
+        row[2] = ((unsigned long long)smid << 32) | iters;
+        for (int i = 0; i < 5; ++i) row[3 + i] = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl) {
+  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl}.warp_bytes();
+}
+
+template <int CPL, int DQT>
+static cudaError_t launch_lp_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
+  auto kern = search_lp_kernel<CPL, DQT>;
+  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL);
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_per_sm = 0, cached_dev = -1;
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  if (cached_smem == smem && cached_dev == dev) {
+    per_sm = cached_per_sm;
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // keep the L1 side large (in-flight gather lines), ask for just enough shared memory for the target residency
+    const int pct = (int)std::min<size_t>(100, (SVF_MINB_LP * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    cached_smem = smem;
+    cached_per_sm = per_sm;
+    cached_dev = dev;
+  }
+  long long blocks = (long long)per_sm * num_sms;
+  const long long need = (a.nq + kSearchWarpsPerBlock - 1) / kSearchWarpsPerBlock;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, kSearchWarpsPerBlock * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int DQT>
+cudaError_t launch_search_lp_dq(SearchArgs a, int cpl, int num_sms, cudaStream_t st) {
+  switch (cpl) {
+    case 1: return launch_lp_cpl<1, DQT>(a, num_sms, st);
+    case 2: return launch_lp_cpl<2, DQT>(a, num_sms, st);
+    case 4: return launch_lp_cpl<4, DQT>(a, num_sms, st);
+    case 8: return launch_lp_cpl<8, DQT>(a, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace svf

@@ -117,6 +117,50 @@ def test_search_dims_and_metrics_integer(svf, dim, metric, wpq):
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
 
 
+@pytest.mark.parametrize("dim,L,p,bits,metric", [(48, 65, 1, 8, 0), (48, 100, 2, 9, 0), (48, 128, 1, 0, 1),
+                                                  (96, 160, 1, 0, 0), (200, 192, 1, 10, 1), (128, 256, 4, 8, 0),
+                                                  (48, 384, 2, 0, 1), (128, 512, 1, 9, 0), (13, 200, 1, 8, 0)])
+def test_large_pool_kernel_bit_exact(svf, dim, L, p, bits, metric):
+    """K-S-L (pools of more than 64 keys in shared memory, direct-mapped visited cache; search_lp.cuh) is bit-exact
+    against O2 with tombstones, caches small enough to forget (bits 8-10; 0 = automatic), search widths 1-4, L2 and
+    inner product, the D = 96 / 128 / 200 specialisations and the generic path, a ragged batch; the iteration and
+    expansion counters are equal and distances are never skipped (only recomputed)."""
+    gen = GLM(dim=dim, ell=8, integer=True)
+    X = gen.rows(9, 9, 0, 6000)
+    Q = gen.rows(9, 10, 0, 333)
+    g, _ = oracle.build(X, R=32, seed_size=1000, B_ins=1000, L_ins=64)
+    dead = random_tombstones(6000, 0.1, seed=L)
+    tomb = pack_tomb(dead, 6000)
+    idx = svf.Index.from_state(X, g, tomb=tomb, metric=metric, search_width=p)
+    idx.set_search_params(p, 0, 0, bits)
+    ids, d = idx.search(cuda(Q), 10, L)
+    cnt = idx.last_search_counters()
+    ri, rd, rc = oracle.graph_search(X, g, Q, 10, L, p=p, metric=metric, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+    assert cnt["iters"] == rc[:, 2].sum() and cnt["n_exp"] == rc[:, 1].sum()
+    assert cnt["n_dist"] >= rc[:, 0].sum()
+    assert not np.isin(u32(ids), dead).any()
+    # insert mode (the whole pool is emitted) goes through the same kernel: svf_insert below is checked end to end
+    # by test_insert_bit_exact_integer_data; here the pool's tail order is checked via k = L
+    ids, d = idx.search(cuda(Q), L, L)
+    ri, rd, _ = oracle.graph_search(X, g, Q, L, L, p=p, metric=metric, tomb=tomb)
+    assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+def test_two_new_vertices_in_one_sub_batch(svf):
+    """The hand-derived sub-batch pin of tests/test_oracle_pins.py through svf_insert: inserted together, vertex 5
+    does not reach vertex 4 although 4 is its nearest (snapshot semantics, I13); the rows and reverse edges equal the
+    hand-derived graph."""
+    from test_oracle_pins import TWO_NEW, two_new_inputs
+
+    X, G, E = two_new_inputs()
+    idx = svf.Index.from_state(X[:4], G[:4], E[:4], capacity=6, protect_prefix=1, insert_itopk=4)
+    ids = idx.insert(X[4:])
+    st = idx.export()
+    assert ids.tolist() == [4, 5]
+    assert st["graph"].tolist() == TWO_NEW["graph"] and st["edge_dist"].tolist() == TWO_NEW["edge_dist"]
+
+
 def test_search_float_data_recall_parity(svf):
     gen = GLM(dim=128, ell=32, s=1.0, m=0.0, sigma=0.05)
     X = gen.rows(3, 3, 0, 20000)
@@ -355,7 +399,7 @@ def c1r64():
     return X, g, e
 
 
-@pytest.mark.parametrize("L,pct", [(32, 100), (32, 30), (14, 50), (128, 100), (64, 0)])
+@pytest.mark.parametrize("L,pct", [(32, 100), (32, 30), (14, 50), (64, 100), (64, 0)])
 def test_search_handoff_bit_exact(svf, c1r64, L, pct):
     """Pair-mode handoff of the batch's stragglers (svf_set_search_handoff): queries suspended by the one-warp grid
     and resumed by the chained pair-mode grid (pool + counters carried over, visited table rebuilt from the pool,
@@ -400,7 +444,8 @@ def test_search_handoff_ip_metric(svf):
 
 def test_search_handoff_mixed_pool_sizes(svf, c1r64):
     """Handoff slots are shared by every pool size of an index: alternating itopk (different register layouts of
-    the suspended pools) must never leave a stale slot that a later launch mistakes for a published one."""
+    the suspended pools) must never leave a stale slot that a later launch mistakes for a published one.  Pools of
+    more than 64 keys run on K-S-L (one grid, no handoff) in between."""
     X, g, e = c1r64
     from workloads import query_rows as qr
 
@@ -411,7 +456,7 @@ def test_search_handoff_mixed_pool_sizes(svf, c1r64):
     for L in (128, 32, 96, 16, 128, 14):
         ids, d = idx.search(cuda(Qb), 10, L)
         ri, rd, _ = oracle.graph_search(X, g, Qb, 10, L)
-        assert idx.last_search_counters()["launches"] == 2
+        assert idx.last_search_counters()["launches"] == (1 if L > 64 else 2)
         assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd), L
 
 
@@ -453,22 +498,44 @@ def test_search_overlapping_insert_on_two_streams(svf, c1):
     assert np.array_equal(u32(ids2), ri) and np.array_equal(f32(d2), rd)
 
 
-@pytest.mark.parametrize("R,frac", [(32, 0.25), (64, 0.3), (16, 0.6)])
-def test_consolidate_bit_exact(svf, R, frac):
-    """NEXT-4 global consolidation (svf_consolidate) equals oracle.consolidate bit for bit (rows and
-    edge distances, integer data), incl. degree 64 (c = 64: the chunked candidate union with a 2^13-slot set)."""
+@pytest.mark.parametrize("R,P,frac", [(32, 16, 0.25), (64, 32, 0.3), (16, 8, 0.6), (64, 0, 0.2), (32, 0, 0.4),
+                                     (128, 64, 0.2), (128, 16, 0.1)])
+def test_consolidate_bit_exact(svf, R, P, frac):
+    """NEXT-4 global consolidation (svf_consolidate, reading C2) equals oracle.consolidate bit for bit
+    (rows and edge distances, integer data): degrees 16-128, protected prefixes 0..R/2 (tails of 16..112 slots), the
+    chunked union of up to R deleted neighbours' lists with its 2^13-slot set."""
     X = GLM(dim=32, ell=8, integer=True).rows(5, 5, 0, 5000)
-    G, E = oracle.build(X, R=R, seed_size=600, B_ins=500, L_ins=128)
-    dead = random_tombstones(5000, frac, seed=R)
+    G, E = oracle.build(X, R=R, P=P, seed_size=600, B_ins=500, L_ins=128)
+    dead = random_tombstones(5000, frac, seed=R + P)
     tomb = pack_tomb(dead, 5000)
-    idx = svf.Index.from_state(X, G, E, tomb=tomb)
+    idx = svf.Index.from_state(X, G, E, tomb=tomb, protect_prefix=P)
     n = idx.consolidate()
     st = idx.export()
-    g2, e2, n2 = oracle.consolidate(X, G, E, tomb)
+    g2, e2, n2 = oracle.consolidate(X, G, E, tomb, P=P)
     assert n == n2 > 0
     assert np.array_equal(st["graph"], g2) and np.array_equal(st["edge_dist"], e2)
     live = np.setdiff1d(np.arange(5000), dead)
     assert not np.isin(st["graph"][live], dead).any()
+
+
+def test_consolidate_hand_example(svf):
+    """The hand-derived refill example of tests/test_oracle_pins.py (x = 0,1,2,3,5,8,13, R=4, P=2, ids 2 and 3
+    deleted) through svf_consolidate: refilled prefix slots, a prefix slot left empty, kept tail entries, tail
+    vacancies filled in key order."""
+    from test_oracle_pins import test_consolidate_hand_example_refill_rules as hand
+
+    class Via:  # routes the pin's consolidate call through the C ABI; everything else stays the oracle's
+        def __init__(self):
+            self.dist = oracle.dist
+
+        def consolidate(self, X, G, E, tomb, P):
+            idx = svf.Index.from_state(X, G, E, tomb=tomb, protect_prefix=P)
+            n = idx.consolidate()
+            st = idx.export()
+            idx.close()
+            return st["graph"], st["edge_dist"], n
+
+    hand(Via())
 
 
 def test_consolidation_triggers_after_deletion_ratio(svf, c1):

@@ -368,6 +368,43 @@ def test_insert_matches_build_growth(orc):
     assert np.array_equal(gi, gb) and np.array_equal(ei, eb)
 
 
+TWO_NEW = {  # hand-derived (docstring of test_two_new_vertices_in_one_sub_batch)
+    "xs": [0, 10, 30, 40, 20, 21],
+    "base_g": [[1, 2], [0, 2], [3, 1], [2, 1]],
+    "graph": [[1, 2], [0, 4], [3, 5], [2, 1], [1, 2], [2, 1]],
+    "edge_dist": [[100, 900], [100, 100], [100, 81], [100, 900], [100, 100], [81, 121]],
+}
+
+
+def two_new_inputs():
+    """Base points x = 0, 10, 30, 40 (ids 0..3, D = 4 zero-padded), R = 2, P = 1, rows = the exact 2-NN (seed
+    layout), then ids 4 (x = 20) and 5 (x = 21) inserted together."""
+    xs = TWO_NEW["xs"]
+    X = np.zeros((6, 4), np.float32)
+    X[:, 0] = xs
+    G = np.full((6, 2), SENT, np.uint32)
+    E = np.full((6, 2), np.inf, np.float32)
+    G[:4] = TWO_NEW["base_g"]
+    E[:4] = [[(xs[v] - xs[u]) ** 2 for u in G[v]] for v in range(4)]
+    return X, G, E
+
+
+def test_two_new_vertices_in_one_sub_batch(orc):
+    """Sub-batch snapshot semantics (I13, "delayed graph updates"): vertices inserted in one sub-batch
+    neither reach nor sample each other.  By hand (L_insert = 4 covers every live id, squared distances):
+      v=4 (x=20): C = [1:100, 2:100, 0:400, 3:400]; detour counts 0,1 (2 in row 1),1 (0 in row 1),1 (3 in row 2)
+                  -> selected 1, 2 -> row [1 | 2] (100 | 100);
+      v=5 (x=21): its nearest vertex is 4 (d 1) but 4 is not in the snapshot: C = [2:81, 1:121, 3:361, 0:441];
+                  counts 0,1,1,1 -> row [2 | 1] (81 | 121);
+      reverse: row 1 tail {2:900} u {4:100, 5:121} -> 4; row 2 tail {1:900} u {4:100, 5:81} -> 5.
+    With sub-batches of one vertex, 5 does see 4 (its first candidate, d 1)."""
+    X, G, E = two_new_inputs()
+    g2, e2 = orc.insert(X, G, E, n_alloc=4, n_new=2, P=1, L_ins=4, B_ins=4096)
+    assert g2.tolist() == TWO_NEW["graph"] and e2.tolist() == TWO_NEW["edge_dist"]
+    g1, _ = orc.insert(X, G, E, n_alloc=4, n_new=2, P=1, L_ins=4, B_ins=1)
+    assert 4 in g1[5].tolist() and 4 not in g2[5].tolist()
+
+
 # ---- O6 shard merge / O7 recall -------------------------------------------------------------------------------------
 def test_shard_merge_identical_for_any_gpu_count(orc):
     S, nq, k = 8, 30, 10
@@ -394,6 +431,27 @@ def test_shard_merge_identical_for_any_gpu_count(orc):
 def test_spec_recall_examples(orc):
     for res, gt, want in golden("spec_examples.json")["recall"]["cases"]:
         assert abs(orc.recall_ids([res], [gt], 3) - want) < 1e-12
+
+
+def test_recall_tie_aware_hand_cases(orc):
+    """O7 tie-aware recall (P:L736 Recall@k): result i counts when its exact distance is <= the
+    k-th true distance (relative slack 1e-5).  Hand cases: an exact tie at the k-th distance counts even with a
+    different id (id recall 2/3, tie-aware 1); a result just beyond the slack does not; negative inner-product
+    distances loosen toward zero (-8 -> -7.99992), never away from it; padded (+inf) results never count; a k-th
+    distance of 0 admits only 0."""
+    ids_gt, d_gt = [[7, 8, 9]], [[1.0, 2.0, 3.0]]
+    assert orc.recall_ids([[7, 8, 4]], ids_gt, 3) == pytest.approx(2 / 3)
+    assert orc.recall_tie_aware([[1.0, 2.0, 3.0]], d_gt, 3) == 1.0
+    assert orc.recall_tie_aware([[1.0, 2.0, 3.0001]], d_gt, 3) == pytest.approx(2 / 3)
+    assert orc.recall_tie_aware([[1.0, 2.0, 3.00002]], d_gt, 3) == 1.0
+    neg = [[-10.0, -9.0, -8.0]]
+    assert orc.recall_tie_aware([[-10.0, -8.0, -7.99995]], neg, 3) == 1.0
+    assert orc.recall_tie_aware([[-10.0, -8.0, -7.9999]], neg, 3) == pytest.approx(2 / 3)
+    assert orc.recall_tie_aware([[1.0, np.inf, np.inf]], d_gt, 3) == pytest.approx(1 / 3)
+    assert orc.recall_tie_aware([[0.0, 0.0, 1e-6]], [[0.0, 0.0, 0.0]], 3) == pytest.approx(2 / 3)
+    # two queries average; only the first k columns are read
+    assert orc.recall_tie_aware([[1.0, 5.0, 0.0], [2.0, 2.0, 9.0]], [[1.0, 2.0, 0.0], [2.0, 3.0, 0.0]],
+                                2) == pytest.approx(3 / 4)
 
 
 # ---- NEXT-1 localized repair ----------------------------------------------------------------------------------------
@@ -461,12 +519,13 @@ def test_repair_properties_on_a_built_graph(orc):
         assert len(set(new) - allowed) <= c * len(per_p)            # O(cR) added edges
 
 
-# ---- NEXT-4 global consolidation (reading C1) -------------------------------------------------------
-def test_consolidate_hand_example(orc):
-    """Points 0,1,2,3,4,10 on a line (D=4, zero-padded), R=2, P=1; vertex 2 deleted.  By hand: the live rows
-    holding 2 are 0, 1 and 3.  Row 0: live {1 (d 1)} + N_out(2) = {1, 3} minus taken/self -> 3 (d 9); detour
-    counts on the starting rows are 0 and 0 -> [1 | 3].  Row 1: {0 (1)} + {3 (4)} (1 itself skipped) -> [0 | 3].
-    Row 3: {4 (1)} + {1 (4)} (3 itself skipped) -> [4 | 1].  Rows 2 (deleted), 4 and 5 are untouched."""
+# ---- NEXT-4 global consolidation (reading C2) -------------------------------------------------------
+def test_consolidate_hand_example_line(orc):
+    """Points 0,1,2,3,4,10 on a line (D=4, zero-padded), R=2, P=1; vertex 2 deleted; N_out(2) = {1, 3}.  By hand:
+    row 0 = [1 | 2]: the live prefix 1 stays, the tail vacancy takes the nearest of U = {3} -> [1 | 3] (d 1, 9).
+    Row 1 = [2 | 0]: the deleted prefix slot takes the nearest member of N_out(2) other than 1 itself -> 3 (d 4);
+    the live tail 0 stays -> [3 | 0].  Row 3 = [2 | 4]: prefix <- 1 (d 4; 3 itself skipped), tail 4 stays ->
+    [1 | 4].  Rows 2 (deleted), 4 and 5 (no deleted neighbour) are untouched."""
     xs = [0, 1, 2, 3, 4, 10]
     X = np.zeros((6, 4), np.float32)
     X[:, 0] = xs
@@ -475,17 +534,48 @@ def test_consolidate_hand_example(orc):
     tomb = pack_tomb(np.array([2], np.uint32), 6)
     g2, e2, n = orc.consolidate(X, G, E, tomb, P=1)
     assert n == 3
-    exp_g = np.array([[1, 3], [0, 3], [1, 3], [4, 1], [3, 5], [4, 3]], np.uint32)
-    exp_e = np.array([[1, 9], [1, 4], E[2], [1, 4], E[4], E[5]], np.float32)
+    exp_g = np.array([[1, 3], [3, 0], [1, 3], [1, 4], [3, 5], [4, 3]], np.uint32)
+    exp_e = np.array([[1, 9], [4, 1], E[2], [4, 1], E[4], E[5]], np.float32)
+    assert np.array_equal(g2, exp_g) and np.array_equal(e2, exp_e)
+
+
+def test_consolidate_hand_example_refill_rules(orc):
+    """x = 0,1,2,3,5,8,13 (ids 0..6), R=4, P=2, ids 2 and 3 deleted; N_out(2) = [5,1,6,0], N_out(3) = [5,4,2,6].
+    Worked by hand (squared distances):
+      row 0 [4,2|1,3]: U = {5:64, 6:169}; prefix slot 1 (p=2) <- 5; the tail keeps 1 and its vacancy takes 6
+                       -> [4,5|1,6] (25,64 | 1,169);
+      row 1 [3,0|2,-]: U = {5:49, 4:16, 6:144}; prefix slot 0 (p=3) <- 4; both tail slots vacant <- 5, 6
+                       -> [4,0|5,6] (16,1 | 49,144);
+      row 4 [3,5|-,-]: U = {6:64}; prefix slot 0 <- 6; nothing left for the tail -> [6,5|-,-];
+      row 5 [2,3|4,-]: U = {1:49, 6:25, 0:64}; slot 0 (p=2) <- 6; slot 1 (p=3): N_out(3) has only 6 (taken)
+                       -> empty; tail keeps 4 and its empty slot takes 1 -> [6,-|4,1] (25,inf | 9,49);
+      row 6 has no deleted neighbour; rows 2, 3 are deleted: all three untouched."""
+    xs = [0, 1, 2, 3, 5, 8, 13]
+    X = np.zeros((7, 4), np.float32)
+    X[:, 0] = xs
+    S, inf = SENT, np.inf
+    G = np.array([[4, 2, 1, 3], [3, 0, 2, S], [5, 1, 6, 0], [5, 4, 2, 6], [3, 5, S, S], [2, 3, 4, S],
+                  [5, 4, S, S]], np.uint32)
+    E = np.array([[(xs[v] - xs[u]) ** 2 if u != S else inf for u in G[v]] for v in range(7)], np.float32)
+    tomb = pack_tomb(np.array([2, 3], np.uint32), 7)
+    g2, e2, n = orc.consolidate(X, G, E, tomb, P=2)
+    assert n == 4
+    exp_g = G.copy()
+    exp_e = E.copy()
+    exp_g[0], exp_e[0] = [4, 5, 1, 6], [25, 64, 1, 169]
+    exp_g[1], exp_e[1] = [4, 0, 5, 6], [16, 1, 49, 144]
+    exp_g[4], exp_e[4] = [6, 5, S, S], [64, 9, inf, inf]
+    exp_g[5], exp_e[5] = [6, S, 4, 1], [25, inf, 9, 49]
     assert np.array_equal(g2, exp_g) and np.array_equal(e2, exp_e)
 
 
 def test_consolidate_properties_on_a_built_graph(orc):
     """After consolidation no live row references a deleted vertex (the defining effect: all affected
-    neighbourhoods); only rows that held a deleted id change; new entries come from the row itself or from the
-    deleted neighbours' lists; deleted rows are frozen; every row keeps the prefix/tail layout."""
+    neighbourhoods); only rows that held a deleted id change, and they keep every live entry (prefix entries in
+    their slots); a refilled prefix slot holds a member of its own deleted neighbour's list; tail refills come from
+    the deleted neighbours' lists and are the nearest such candidates not used elsewhere; deleted rows are frozen."""
     X = GLM(dim=16, ell=6, integer=True).rows(8, 8, 0, 3000)
-    R = 16
+    R, P = 16, 8
     G, E = orc.build(X, R=R, seed_size=500, B_ins=400, L_ins=48)
     dead = random_tombstones(3000, 0.25, seed=11)
     tomb = pack_tomb(dead, 3000)
@@ -499,16 +589,37 @@ def test_consolidate_properties_on_a_built_graph(orc):
     unaff = np.setdiff1d(live, affected)
     assert np.array_equal(g2[unaff], G[unaff])
     for v in affected[:300]:
-        old = [int(x) for x in G[v] if x != SENT]
-        pool = set(x for x in old if x not in deadset)
-        for p in old:
-            if p in deadset:
-                pool |= set(int(x) for x in G[p] if x != SENT and int(x) not in deadset and int(x) != v)
-        new = [int(x) for x in g2[v] if x != SENT]
-        assert set(new) <= pool and v not in new and len(set(new)) == len(new)
-        assert len(new) == min(R, len(pool))
-        tail = [(float(e2[v, s]), int(g2[v, s])) for s in range(R // 2, R) if g2[v, s] != SENT]
-        assert tail == sorted(tail)
-    # consolidation equals repair with every deleted neighbour's whole list at threshold 0
-    g3, e3, n3, _ = orc.repair(X, G, E, tomb, c=R, threshold=0.0)
-    assert np.array_equal(g2, g3) and np.array_equal(e2, e3) and n3 == n
+        old = [int(x) for x in G[v]]
+        lists = {p: set(int(x) for x in G[p] if x != SENT) for p in old if p in deadset}
+        cand = set().union(*lists.values()) - deadset - {v} - set(old)
+        for s in range(P):
+            if old[s] == SENT or old[s] not in deadset:
+                assert g2[v, s] == G[v, s] and e2[v, s] == E[v, s]          # live prefix entries stay in place
+            elif g2[v, s] != SENT:
+                assert int(g2[v, s]) in lists[old[s]] and int(g2[v, s]) in cand
+        kept = {(float(E[v, s]), old[s]) for s in range(P, R) if old[s] != SENT and old[s] not in deadset}
+        tail = [(float(e2[v, s]), int(g2[v, s])) for s in range(P, R) if g2[v, s] != SENT]
+        assert tail == sorted(tail) and kept <= set(tail)                  # live tail entries kept, tail sorted
+        refills = [t for t in tail if t not in kept]
+        assert all(x in cand for _, x in refills)
+        used = set(int(x) for x in g2[v] if x != SENT)
+        others = [(float(orc.dist(X[v], X[x])), x) for x in cand - used]
+        if refills and others:
+            assert max(refills) < min(others)                               # the nearest unused candidates
+        if len(tail) < R - P:
+            assert not others                                               # vacancies stay only when U ran out
+        assert v not in used and len(used) == len([x for x in g2[v] if x != SENT])
+
+
+# ---- O4 lazy deletion -------------------------------------------------------------------------------
+def test_delete_sets_bits_idempotently(orc):
+    """Bits are set per id (bit id%32 of word id/32, the layout include/svf.h states), a repeated id or an already
+    deleted id is not counted again (S:L389 idempotent no-op), an id >= n_alloc deletes nothing."""
+    t0 = np.zeros(3, np.uint32)
+    t1, newly = orc.delete(t0, [0, 31, 32, 70, 31], n_alloc=80)
+    assert newly == 4 and t1.tolist() == [1 | (1 << 31), 1, 1 << 6]
+    t2, newly2 = orc.delete(t1, [70, 5], n_alloc=80)
+    assert newly2 == 1 and t2.tolist() == [1 | (1 << 31) | (1 << 5), 1, 1 << 6]
+    with pytest.raises(KeyError):
+        orc.delete(t2, [3, 80], n_alloc=80)
+    assert t2.tolist() == [1 | (1 << 31) | (1 << 5), 1, 1 << 6]

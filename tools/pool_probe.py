@@ -1,0 +1,89 @@
+"""Where does a large-pool search spend its time?  Per-query timelines (svf_set_trace) of itopk >= 128 searches on
+the C2 graph (the insert search's shape: L_insert = 128 over 4096-query sub-batches), with per-phase SM cycles when
+the library is the -DSVF_PHASE_PROF variant (SVF_LIB=...).  Also times one 10K insert with its stage breakdown.
+
+  SVF_LIB=paper_2601_08528_b200/libsvf_phase.so python tools/pool_probe.py --out gpurun_out/pool_probe.json
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2601_08528_b200 as svf  # noqa: E402
+from tools.tail_trace import analyse  # noqa: E402
+from workloads import base_rows  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--build-itopk", type=int, default=256)
+    ap.add_argument("--itopks", default="128,192,256")
+    ap.add_argument("--batches", default="4096,10000")
+    ap.add_argument("--width", type=int, default=1)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    dev = torch.device("cuda:0")
+    X = base_rows(a.config)
+    n = len(X)
+    idx = svf.Index.build(torch.from_numpy(X).to(dev), degree=64, capacity=n + 40_000, build_itopk=a.build_itopk)
+    Qn = torch.from_numpy(base_rows(a.config, n, 20_000)).to(dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    res = {"config": f"{a.config} graph at L_build {a.build_itopk}; queries = fresh insert vectors", "runs": []}
+    idx.set_search_handoff(0)
+    for L in [int(x) for x in a.itopks.split(",")]:
+        for nq in [int(x) for x in a.batches.split(",")]:
+            idx.set_search_params(a.width, 0, 0, 0)
+            Q = Qn[:nq].contiguous()
+            for _ in range(2):
+                idx.search(Q, 10, L)
+            ts = []
+            for _ in range(5):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                idx.search(Q, 10, L)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            c = idx.last_search_counters()
+            idx.set_trace(True)
+            flush.zero_()
+            idx.search(Q, 10, L)
+            torch.cuda.synchronize()
+            r = analyse(*idx.read_trace(nq))
+            idx.set_trace(False)
+            row = {"itopk": L, "nq": nq, "width": a.width, "ms_median": round(float(np.median(ts)), 4),
+                   "n_dist_per_q": round(c["n_dist"] / c["queries"], 1), "iters_per_q": round(c["iters"] / c["queries"], 1),
+                   **{k: r[k] for k in ("span_us", "drain_us", "after_drain_us", "dur_us", "ns_per_iter_median",
+                                        "phase_cycles_per_iter")}}
+            row["hbm_frac_alg"] = round(nq * (c["n_dist"] / c["queries"] * X.shape[1] * 4) / (row["ms_median"] * 1e-3)
+                                        / 6545e9, 4)
+            print(json.dumps(row), flush=True)
+            res["runs"].append(row)
+    idx.set_search_handoff(-1)
+    idx.set_search_params(1, 0, 0, 0)
+    idx.profile(True)
+    tt = []
+    for j in range(4):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        idx.insert(Qn[(j % 2) * 10_000:(j % 2 + 1) * 10_000])
+        e1.record()
+        torch.cuda.synchronize()
+        tt.append(e0.elapsed_time(e1))
+    pr = idx.profile_read()
+    res["insert_10k_ms"] = [round(t, 3) for t in tt]
+    res["insert_breakdown_ms_per_batch"] = {k: round(v[0] / 4, 3) for k, v in pr.items()}
+    print(json.dumps({k: res[k] for k in ("insert_10k_ms", "insert_breakdown_ms_per_batch")}), flush=True)
+    if a.out:
+        json.dump(res, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
