@@ -152,7 +152,7 @@ int pow2_at_least(int x) {
 }
 
 struct SearchCfg {
-  int kpl, cpl, hbits, team, nv, n_init, wpq, lp;
+  int kpl, cpl, hbits, team, nv, n_init, wpq, lp, vc_bits;
 };
 
 // K-S-L (shared-memory pool kernel) for pools of more than 64 keys; SVF_LP=0 keeps the register-pool kernel (A/B)
@@ -160,6 +160,14 @@ bool lp_enabled() {
   static const bool on = [] {
     const char* v = getenv("SVF_LP");
     return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+// SVF_LP_U32=1 forces u32 cache entries (A/B of the 16-bit tagged cache)
+bool lp_u32_cache() {
+  static const bool on = [] {
+    const char* v = getenv("SVF_LP_U32");
+    return v != nullptr && atoi(v) != 0;
   }();
   return on;
 }
@@ -193,16 +201,22 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   // K-S-L for pools of more than 64 keys (one warp per query): its direct-mapped visited cache needs no load
   // invariant, only room to stage the query row
   c.lp = LP > 64 && idx->wpq != 2 && lp_enabled();
+  c.vc_bits = 0;
   if (c.lp) {
     int lpmin = 8;
-    while ((1 << lpmin) < idx->Dp) ++lpmin;
+    while ((1 << lpmin) < 2 * idx->Dp) ++lpmin;  // the cache region (>= 2 bytes per slot) stages the query row
     c.hbits = std::max(hash_bits > 0 ? hash_bits : lp_bits_auto(L), lpmin);
+    // 16-bit tagged cache entries when every id of the index fits in hbits + 15 bits (exact, DESIGN §6 K-S-L)
+    int B = 1;
+    while (B < 32 && ((int64_t)1 << B) < idx->cap) ++B;
+    B = std::max(B, c.hbits);
+    c.vc_bits = (B - c.hbits <= 15 && !lp_u32_cache()) ? B : 0;
   } else {
     c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   }
   if (c.hbits > 15) return why = "hash_bits too large", false;
   // a configuration whose block does not fit the opt-in shared memory is refused up front (INVALID, index intact)
-  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp) > (size_t)idx->smem_optin)
+  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp, c.vc_bits) > (size_t)idx->smem_optin)
     return why = "hash_bits too large: the search block's visited tables exceed the shared memory per block", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
@@ -348,6 +362,7 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.wpq = c.wpq;
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
   a.large_pool = c.lp && a.wpq == 1;
+  a.vc_bits = c.vc_bits;
   cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   unsigned long long*& hob = update_path ? idx->ho_upd : idx->ho;

@@ -24,11 +24,11 @@ namespace svf {
 
 namespace {
 
-// per-warp shared memory: [cache 2^hbits u32 | pool Lp u64 | survivor ids MP u32 | keys MP u64 | new keys MP u64 |
-// insertion points MP u32 | query slot 2 u64 | parents 8 u32]
+// per-warp shared memory: [visited cache 2^hbits entries (u16 tags or u32 ids) | pool Lp u64 | survivor ids MP u32 |
+// keys MP u64 | new keys MP u64 | (spare) MP u32 | query slot 2 u64 | parents 8 u32]
 struct LpLayout {
-  int hbits, Lp, MP;
-  __host__ __device__ size_t pool_off() const { return (size_t)4 << hbits; }
+  int hbits, Lp, MP, c16;
+  __host__ __device__ size_t pool_off() const { return (((size_t)(c16 ? 2 : 4) << hbits) + 15) & ~(size_t)15; }
   __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
   __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
   __host__ __device__ size_t ck_off() const { return skey_off() + (size_t)MP * 8; }
@@ -38,13 +38,26 @@ struct LpLayout {
 };
 
 #ifndef SVF_MINB_LP
-#define SVF_MINB_LP 6
+#define SVF_MINB_LP 7
 #endif
 #ifndef SVF_GATHER_U_LP
 #define SVF_GATHER_U_LP 2
 #endif
 
-__device__ __forceinline__ uint32_t cache_slot(uint32_t id, int hbits) { return (id * 0x9E3779B1u) >> (32 - hbits); }
+// Visited cache slot and tag of an id.  vc_bits = B > 0: ids are < 2^B and h = id * odd mod 2^B is a bijection of
+// [0, 2^B); the slot is h's top hbits and the tag its low B - hbits bits (+1, so 0 marks an empty slot), stored in 16
+// bits (B - hbits <= 15): equal tags in a slot mean equal ids, so the cache stays exact while holding twice the
+// entries of a u32 cache in the same shared memory.  B = 0: u32 entries holding the id itself (empty = 0xFFFFFFFF).
+__device__ __forceinline__ void cache_pos(uint32_t id, int hbits, int B, uint32_t& slot, uint32_t& tag) {
+  if (B) {
+    const uint32_t h = (id * 0x9E3779B1u) & ((1u << B) - 1u);
+    slot = h >> (B - hbits);
+    tag = (h & ((1u << (B - hbits)) - 1u)) + 1u;
+  } else {
+    slot = (id * 0x9E3779B1u) >> (32 - hbits);
+    tag = id;
+  }
+}
 
 // number of keys in sorted a[0..n) whose flag-stripped value is < k (k has its flag bit clear)
 __device__ __forceinline__ int lower_bound_key(const uint64_t* a, int n, uint64_t k) {
@@ -62,9 +75,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int MP = 32 * CPL;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP};
+  const int VB = a.vc_bits;  // 16-bit tagged cache when > 0
+  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP, VB > 0};
   unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
   uint32_t* cache = reinterpret_cast<uint32_t*>(base);
+  uint16_t* cache16 = reinterpret_cast<uint16_t*>(base);
   uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());
   uint32_t* sid = reinterpret_cast<uint32_t*>(base + lay.sid_off());
   uint64_t* skey = reinterpret_cast<uint64_t*>(base + lay.skey_off());
@@ -101,7 +116,8 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     unsigned long long t_start = 0;
     if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    // S0: stage the query through the cache region (coalesced), keep this lane's fragment, clear the cache
+    // S0: stage the query through the cache region (coalesced; the host keeps it >= Dp floats), keep this lane's
+    // fragment, clear the cache
     const float* qg = a.Q + (size_t)qi * a.q_stride;
     float* qstage = reinterpret_cast<float*>(cache);
     for (int i = lane; i < a.dq * 4; i += 32) qstage[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
@@ -114,15 +130,21 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
                                                                : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncwarp();
-    for (int i = lane; i < H; i += 32) cache[i] = kHashEmpty;
+    if (VB) {
+      for (int i = lane; i < (H >> 1); i += 32) cache[i] = 0u;
+    } else {
+      for (int i = lane; i < H; i += 32) cache[i] = kHashEmpty;
+    }
     __syncwarp();
 
     int np = 0;  // entries in the pool (<= L)
     int fu = 0;  // every entry before fu is parented
     uint32_t n_dist = 0, iters = 0, n_exp = 0;
 
-    // S6 C.Update for the keys skey[0..S): drop those not better than the L-th key, sort, drop duplicates and keys
-    // already in the pool, merge the rest in place
+    // S6 C.Update for the keys skey[0..S): drop those not better than the L-th key, then, 32 at a time, drop repeated
+    // keys and keys already in the pool and merge the rest in place.  No sort: a new key's final position is its
+    // insertion point b (binary search in the pool) plus its rank among the kept new keys (a shuffle count), and a
+    // pool key at position i moves up by the number of kept new keys with b <= i.
     auto update = [&](int S) {
       const uint64_t kth = np < L ? kEmptyKey : (pool[L - 1] & ~1ull);
       int S2 = 0;
@@ -135,70 +157,47 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         if (pass) ck[S2 + __popc(m & ((1u << lane) - 1u))] = k;
         S2 += __popc(m);
       }
-      if (S2 == 0) return;
       __syncwarp();
-      int m = 0;
-      auto dedup_compact = [&](auto& c) {  // c: sorted register array (element e = r*32 + lane)
-        constexpr int E = sizeof(c) / sizeof(c[0]);
-        uint64_t prev_last = kEmptyKey;
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const int e = r * 32 + lane;
-          uint64_t prev = __shfl_up_sync(0xffffffffu, c[r], 1);
-          if (lane == 0) prev = prev_last;
-          prev_last = __shfl_sync(0xffffffffu, c[r], 31);
-          int b = 0;
-          bool keep = e < S2 && !(e > 0 && prev == c[r]);  // equal keys: the same id offered twice (p > 1)
-          if (keep) {
-            b = lower_bound_key(pool, np, c[r]);
-            keep = !(b < np && (pool[b] & ~1ull) == c[r]);  // already in the pool (the cache forgot it)
-          }
-          const unsigned km = __ballot_sync(0xffffffffu, keep);
-          if (keep) {
-            const int j = m + __popc(km & ((1u << lane) - 1u));
-            skey[j] = c[r];
-            cb[j] = (uint32_t)b;
-          }
-          m += __popc(km);
+      for (int base = 0; base < S2; base += 32) {
+        const int nh = min(32, S2 - base);
+        const uint64_t c = lane < nh ? ck[base + lane] : kEmptyKey;
+        int b = L;
+        bool keep = false;
+        if (lane < nh) {
+          b = lower_bound_key(pool, np, c);
+          keep = !(b < np && (pool[b] & ~1ull) == c);  // already in the pool (the cache forgot it)
         }
-      };
-      if (S2 <= 32) {
-        uint64_t c[1];
-        c[0] = lane < S2 ? ck[lane] : kEmptyKey;
-        warp_sort<1>(c, lane);
-        dedup_compact(c);
-      } else {
-        uint64_t c[CPL];
+        for (int i = 0; i < nh; ++i) {                 // the same id offered twice (p > 1): keep the first copy
+          const uint64_t ci = __shfl_sync(0xffffffffu, c, i);
+          if (i < lane && ci == c) keep = false;
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (km == 0u) continue;
+        int rank = 0;
+        for (int i = 0; i < nh; ++i) {
+          const uint64_t ci = __shfl_sync(0xffffffffu, c, i);
+          rank += ((km >> i) & 1u) && ci < c;
+        }
+        int b0 = keep ? b : L;
 #pragma unroll
-        for (int r = 0; r < CPL; ++r) c[r] = r * 32 + lane < S2 ? ck[r * 32 + lane] : kEmptyKey;
-        warp_sort<CPL>(c, lane);
-        dedup_compact(c);
-      }
-      if (m == 0) return;
-      __syncwarp();
-      // pool keys at [b0, np) move up by the number of new keys below them, back-to-front in 32-key chunks
-      const int b0 = (int)cb[0];
-      if (np > b0) {
-        for (int s0 = b0 + ((np - b0 - 1) & ~31); s0 >= b0; s0 -= 32) {
+        for (int off = 16; off > 0; off >>= 1) b0 = min(b0, __shfl_xor_sync(0xffffffffu, b0, off));
+        for (int s0 = b0 + ((np - b0 - 1) & ~31); np > b0 && s0 >= b0; s0 -= 32) {  // back to front
           const int i = s0 + lane;
-          uint64_t pk = 0;
-          int dst = L;
-          if (i < np) {
-            pk = pool[i];
-            dst = i + lower_bound_key(skey, m, pk & ~1ull);
+          int cnt = 0;
+          for (int j = 0; j < nh; ++j) {
+            const int bj = __shfl_sync(0xffffffffu, b, j);
+            cnt += ((km >> j) & 1u) && bj <= i;
           }
+          const uint64_t pk = i < np ? pool[i] : 0ull;
           __syncwarp();
-          if (dst < L) pool[dst] = pk;
+          if (i < np && i + cnt < L) pool[i + cnt] = pk;
           __syncwarp();
         }
+        if (keep && b + rank < L) pool[b + rank] = c;
+        __syncwarp();
+        np = min(L, np + __popc(km));
+        fu = min(fu, b0);
       }
-      for (int j = lane; j < m; j += 32) {
-        const int dst = j + (int)cb[j];
-        if (dst < L) pool[dst] = skey[j];
-      }
-      __syncwarp();
-      np = min(L, np + m);
-      fu = min(fu, b0);
     };
 
     // S1: the first n_init live ids along the seeded affine permutation (I2), scored and merged in chunks
@@ -225,7 +224,10 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           const bool keep = ok && taken + pos < a.n_init;
           if (keep) {
             sid[pos] = id;
-            cache[cache_slot(id, a.hbits)] = id;
+            uint32_t slot, tag;
+            cache_pos(id, a.hbits, VB, slot, tag);
+            if (VB) cache16[slot] = (uint16_t)tag;
+            else cache[slot] = tag;
           }
           running += __popc(m);
         }
@@ -240,6 +242,18 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     // S2-S7: expand the first p unparented entries until every pool entry is parented (I3, I4)
     uint32_t spec_id = kSent;  // parent whose row sits in spec_row (speculative next-row load)
     uint32_t spec_row[CPL];
+#ifdef SVF_PHASE_PROF
+    unsigned long long ph[5] = {0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define SVF_LPH(i)                  \
+  {                                 \
+    const long long tn = clock64(); \
+    ph[i] += tn - tp;               \
+    tp = tn;                        \
+  }
+#else
+#define SVF_LPH(i)
+#endif
     for (;;) {
       if (a.max_iter > 0 && (int)iters == a.max_iter) break;
       // S2 GetNearest: scan from the cursor, mark the first p unparented entries
@@ -274,6 +288,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
       fu = nxt;
       ++iters;
       n_exp += npar;
+      SVF_LPH(0)
       const int ncand = npar * a.R;
       // S3: neighbour rows (from the speculative registers when the guess held), coalesced
       uint32_t rowv[CPL];
@@ -303,6 +318,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           asm volatile("prefetch.global.L2 [%0];" ::"l"(a.graph + (size_t)nid * a.R + lane * 32));
         }
       }
+      SVF_LPH(1)
       // S4: sentinel / snapshot / tombstone / visited-cache filters
       int running = 0;
 #pragma unroll
@@ -310,23 +326,27 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         const uint32_t id = rowv[r];
         bool ok = id != kSent && (uint64_t)id < n;
         if (ok) ok = !tomb_dead(a.tomb, id);
-        uint32_t slot = 0;
+        uint32_t slot = 0, tag = 0;
         if (ok) {
-          slot = cache_slot(id, a.hbits);
-          ok = cache[slot] != id;
+          cache_pos(id, a.hbits, VB, slot, tag);
+          ok = VB ? cache16[slot] != (uint16_t)tag : cache[slot] != tag;
         }
         const unsigned m = __ballot_sync(0xffffffffu, ok);
         if (ok) {
           sid[running + __popc(m & ((1u << lane) - 1u))] = id;
-          cache[slot] = id;
+          if (VB) cache16[slot] = (uint16_t)tag;
+          else cache[slot] = tag;
         }
         running += __popc(m);
       }
+      SVF_LPH(2)
       if (running == 0) continue;
       // S5 distances, S6 merge
       gather_keys<DQT, U>(a, sid, skey, running, qv, lane);
       n_dist += running;
+      SVF_LPH(3)
       update(running);
+      SVF_LPH(4)
     }
 
     // S8: emit the first n_out entries (k, or the whole pool in insert mode)
@@ -350,7 +370,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         row[0] = t_start;
         row[1] = t_end;
         row[2] = ((unsigned long long)smid << 32) | iters;
+#ifdef SVF_PHASE_PROF
+        for (int i = 0; i < 5; ++i) row[3 + i] = ph[i];
+#else
         for (int i = 0; i < 5; ++i) row[3 + i] = 0;
+#endif
       }
     }
     __syncwarp();
@@ -359,14 +383,14 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
 
 }  // namespace
 
-static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl) {
-  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl}.warp_bytes();
+static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl, int c16) {
+  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl, c16}.warp_bytes();
 }
 
 template <int CPL, int DQT>
 static cudaError_t launch_lp_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   auto kern = search_lp_kernel<CPL, DQT>;
-  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL);
+  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL, a.vc_bits > 0);
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0, cached_dev = -1;
   int dev = 0, per_sm = 0;

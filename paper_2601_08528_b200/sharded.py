@@ -102,7 +102,12 @@ class ShardedIndex:
         else:
             import torch.distributed as dist
 
-            dist.all_gather_into_tensor(gathered, pairs.contiguous(), group=self.group)  # rank-major blocks
+            if pairs.is_cuda and dist.get_backend(self.group) == "gloo":   # gloo gathers host tensors (tests)
+                host = gathered.cpu()
+                dist.all_gather_into_tensor(host, pairs.cpu(), group=self.group)
+                gathered.copy_(host)
+            else:
+                dist.all_gather_into_tensor(gathered, pairs.contiguous(), group=self.group)  # rank-major blocks
             gathered = gathered.view(self.world, nq, k)
         return self.merge_pairs_fn(gathered)
 

@@ -25,3 +25,4 @@ def test_sharded_search_multi_process(world):
                          timeout=540)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "sharded exact kNN == single-index exact kNN: True" in out.stdout
+    assert "G=1 search: True" in out.stdout

@@ -560,3 +560,55 @@ def test_consolidation_triggers_after_deletion_ratio(svf, c1):
     ids, d = idx.search(cuda(Q), 10, 32)
     ri, rd, _ = oracle.graph_search(X, g2, Q, 10, 32, tomb=tomb)
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+
+
+# ---- 8 logical shards, rank pre-merge, merge of the gathered pairs ------------------------------------
+def test_sharded_8_shards_equal_oracle_o6_for_every_grouping(svf):
+    """O6: shard s holds global ids g with g mod 8 = s (local id g div 8); the merged answer is O2 per shard with ids
+    mapped back, then the first k of the merge by key.  The 8 shards in one process, grouped as G = 1, 2, 4, 8 ranks
+    (svf_shard_premerge per rank, then svf_merge_pairs over the G rank blocks, i.e. what the all-gather feeds), give
+    that answer bit for bit; so does exact kNN (equal to O1 over the whole set).  Ties across shards (integer data)
+    resolve by the lower global id."""
+    from paper_2601_08528_b200.sharded import ShardedIndex, owned_shards
+
+    gen = GLM(dim=32, ell=8, integer=True)
+    X = gen.rows(13, 13, 0, 16_000)
+    Q = gen.rows(13, 14, 0, 300)
+    S, k, L = 8, 10, 48
+    shards = {s: svf.Index.from_state(X[s::S], oracle.build(X[s::S], R=16, seed_size=500, B_ins=500, L_ins=48)[0])
+              for s in range(S)}
+    ri_s, rd_s = [], []
+    for s in range(S):
+        st = shards[s].export()
+        i, d, _ = oracle.graph_search(X[s::S], st["graph"], Q, k, L)
+        ri_s.append(np.where(i == SENT, SENT, i.astype(np.int64) * S + s).astype(np.uint32))
+        rd_s.append(d)
+    want_i, want_d = oracle.merge_topk(np.stack(ri_s), np.stack(rd_s))
+    Qd = cuda(Q)
+    for G in (1, 2, 4, 8):
+        blocks = []
+        for r in range(G):
+            mine = owned_shards(S, r, G)
+            ids_l = torch.empty((len(mine), len(Q), k), dtype=torch.int32, device="cuda")
+            d_l = torch.empty((len(mine), len(Q), k), dtype=torch.float32, device="cuda")
+            for i, s in enumerate(mine):
+                shards[s].search_into(Qd, k, L, ids_l[i], d_l[i])
+            blocks.append(svf.shard_premerge(ids_l, d_l, S, mine))
+        mi, md = svf.merge_pairs(torch.stack(blocks))
+        assert np.array_equal(u32(mi), want_i) and np.array_equal(f32(md), want_d), G
+    sh = ShardedIndex(shards, S)
+    gi, gd = sh.knn_exact(Qd, k)
+    oi, od = oracle.bf_knn(X, Q, k)
+    assert np.array_equal(u32(gi), oi) and np.array_equal(f32(gd), od)
+    si, sd = sh.search(Qd, k, L)
+    assert np.array_equal(u32(si), want_i) and np.array_equal(f32(sd), want_d)
+    # routed updates: a global batch lands on the owning shards with local ids g div 8; deletes route the same way
+    Xn = gen.rows(13, 15, 0, 20)
+    shards2 = {s: svf.Index.from_state(X[s::S], shards[s].export()["graph"], capacity=len(X[s::S]) + 3)
+               for s in range(S)}
+    sh2 = ShardedIndex(shards2, S)
+    mine = sh2.insert(Xn, len(X))
+    assert mine.tolist() == list(range(len(X), len(X) + 20))
+    assert sh2.delete(np.array([3, 16_003, 16_019, 9], np.uint32)) == 4
+    ids3, _ = sh2.search(Qd, k, L)
+    assert not np.isin(u32(ids3), [3, 16_003, 16_019, 9]).any()

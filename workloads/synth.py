@@ -55,10 +55,11 @@ class GLM:
         mu, w, delta = self._model(model_seed)
         if ood:
             mu = mu + delta[None, :]
+        w32 = w.astype(np.float32)
         out = np.empty((n, self.dim), dtype=np.float32)
-        pos = 0
         b0, b1 = start // BLOCK, (start + n - 1) // BLOCK if n > 0 else start // BLOCK - 1
-        for b in range(b0, b1 + 1):
+
+        def block(b):  # rows of Philox block b that fall in [start, start + n): independent of every other block
             g = _rng(row_seed, _ROW_STREAM, b)
             comp = g.integers(0, self.n_comp, size=BLOCK)
             eps = g.standard_normal((BLOCK, self.ell), dtype=np.float32)
@@ -66,14 +67,31 @@ class GLM:
             lo = max(start, b * BLOCK) - b * BLOCK
             hi = min(start + n, (b + 1) * BLOCK) - b * BLOCK
             z = mu[comp[lo:hi]].astype(np.float32) + 0.6 * eps[lo:hi]
-            x = self.s * (z @ w.astype(np.float32)) + self.m + self.sigma * eta[lo:hi]
+            x = self.s * (z @ w32) + self.m + self.sigma * eta[lo:hi]
             if self.integer:
                 x = np.clip(np.rint(x), 0, 255)
             if self.normalize:
                 x = x / np.maximum(np.linalg.norm(x, axis=1, keepdims=True), 1e-30)
+            pos = b * BLOCK + lo - start
             out[pos:pos + hi - lo] = x
-            pos += hi - lo
+
+        _for_blocks(block, b0, b1)
         return out
+
+
+def _for_blocks(fn, b0: int, b1: int) -> None:
+    """fn(b) for every block b0..b1; blocks are independent Philox streams, so large ranges run on a thread pool
+    (numpy releases the GIL while filling) with bit-identical output."""
+    nb = b1 - b0 + 1
+    if nb <= 1:
+        for b in range(b0, b1 + 1):
+            fn(b)
+        return
+    import concurrent.futures
+    import os
+
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(nb, os.cpu_count() or 1, 16)) as ex:
+        list(ex.map(fn, range(b0, b1 + 1)))
 
 
 @dataclasses.dataclass(frozen=True)
