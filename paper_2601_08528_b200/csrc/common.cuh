@@ -106,4 +106,29 @@ __device__ __forceinline__ void warp_merge_into(uint64_t (&pool)[EP], const uint
   warp_bitonic_merge<EP>(pool, lane);
 }
 
+// ---- 1-D bulk copies (TMA unit) into shared memory, completed on an mbarrier --------------------------------------
+__device__ __forceinline__ uint32_t bulk_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bulk_smem_u32(b)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// dst, src 16-byte aligned, bytes a multiple of 16; one thread issues; the mbarrier's phase completes on arrival
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bulk_smem_u32(b)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   bulk_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(bulk_smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "BW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra BW_%=;\n}" ::"r"(bulk_smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
 }  // namespace svf

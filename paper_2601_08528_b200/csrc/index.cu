@@ -203,8 +203,7 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.lp = LP > 64 && idx->wpq != 2 && lp_enabled();
   c.vc_bits = 0;
   if (c.lp) {
-    int lpmin = 8;
-    while ((1 << lpmin) < 2 * idx->Dp) ++lpmin;  // the cache region (>= 2 bytes per slot) stages the query row
+    const int lpmin = 8;
     c.hbits = std::max(hash_bits > 0 ? hash_bits : lp_bits_auto(L), lpmin);
     // 16-bit tagged cache entries when every id of the index fits in hbits + 15 bits (exact, DESIGN §6 K-S-L)
     int B = 1;
@@ -216,7 +215,7 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   }
   if (c.hbits > 15) return why = "hash_bits too large", false;
   // a configuration whose block does not fit the opt-in shared memory is refused up front (INVALID, index intact)
-  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp, c.vc_bits) > (size_t)idx->smem_optin)
+  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp, c.vc_bits, idx->Dp) > (size_t)idx->smem_optin)
     return why = "hash_bits too large: the search block's visited tables exceed the shared memory per block", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
@@ -382,8 +381,8 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   }
   idx->last_launches = a.ho != nullptr ? 2 : 1;
   if (e != cudaSuccess) return e;
-  cudaEvent_t pa;
-  prof_begin(idx, st, &pa);
+  cudaEvent_t pa = nullptr;
+  if (prof_slot >= 0) prof_begin(idx, st, &pa);
   e = launch_search(a, c.kpl, c.cpl, idx->num_sms, st);
   if (e != cudaSuccess) return e;
   prof_end(idx, st, pa, prof_slot);
@@ -509,20 +508,46 @@ svf_status insert_present_rows(svf_index* idx, int64_t n, int L, cudaStream_t st
   return SVF_OK;
 }
 
-// exact kNN over ids [0, n): tcgen05 TF32 path when supported, else the FFMA tile kernel
+// the exact-kNN pruning bound from a short graph search (DESIGN §6 K-G); SVF_KNN_BOUND=0 keeps the sample pass (A/B)
+bool knn_graph_bound() {
+  static const bool on = [] {
+    const char* v = getenv("SVF_KNN_BOUND");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
+// exact kNN over ids [0, n): tcgen05 TF32 path when supported, else the FFMA tile kernel.  With a built graph over
+// those ids (svf_knn_exact), a capped K-S search first gives k live rows per query whose exact k-th distance bounds
+// the true k-th from above: the tensor-core pass prunes with it (any such bound keeps the result exact: K-R's
+// certificate and the FFMA fallback do not depend on it), replacing the slower sample pass.
 cudaError_t run_knn(svf_index* idx, int64_t n, const uint32_t* tomb, const float* Q, int64_t q_stride, int q_dim,
                     int64_t nq, int k, int64_t self_base, uint32_t* oi, float* od, cudaStream_t st) {
   const bool tc = idx->knn_mode == 0 && knn_tc_supported(idx->dq, q_stride, Q, k);
-  const size_t need = tc ? knn_tc_scratch_bytes(nq, n, idx->dq, k) : knn_scratch_bytes(nq, k, std::max<int64_t>(n, 1));
+  SearchCfg sc{};
+  std::string why;
+  const int Lb = std::max(k, 16);
+  const bool bound = tc && self_base < 0 && n == idx->n_alloc && n >= 262144 && nq >= 512 && knn_graph_bound() &&
+                     Lb <= 64 && search_cfg(idx, Lb, 1, 0, 0, sc, why);
+  const size_t bb = bound ? 2 * al((size_t)nq * k * 4) : 0;
+  const size_t need = bb + (tc ? knn_tc_scratch_bytes(nq, n, idx->dq, k) : knn_scratch_bytes(nq, k, std::max<int64_t>(n, 1)));
   cudaError_t e = ensure_scratch(idx, need, st);
   if (e != cudaSuccess) return e;
   idx->knn_queries += (uint64_t)nq;
   if (!tc)
     return launch_knn_exact(idx->vec, idx->dq, n, tomb, Q, q_stride, q_dim, nq, k, idx->p.metric, self_base, oi, od,
                             idx->scratch, idx->scratch_bytes, idx->num_sms, st);
+  const float* bound_d = nullptr;
+  if (bound) {
+    uint32_t* b_ids = static_cast<uint32_t*>(idx->scratch);
+    float* b_d = reinterpret_cast<float*>(static_cast<char*>(idx->scratch) + bb / 2);
+    e = run_search(idx, Q, q_stride, q_dim, nq, (uint64_t)n, 0, Lb, k, sc, 1, 16, b_ids, b_d, nullptr, -1, st, true);
+    if (e != cudaSuccess) return e;
+    bound_d = b_d;
+  }
   uint32_t fb = 0;
   e = launch_knn_tc(idx->vec, idx->dq, n, tomb, Q, q_stride, q_dim, nq, k, idx->p.metric, self_base, oi, od,
-                    idx->scratch, idx->scratch_bytes, idx->num_sms, st, &fb);
+                    static_cast<char*>(idx->scratch) + bb, idx->scratch_bytes - bb, idx->num_sms, st, &fb, bound_d);
   idx->knn_fallbacks += fb;
   idx->knn_tc_calls += 1;
   return e;

@@ -79,7 +79,7 @@ struct SearchArgs {
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 // dynamic shared memory of one search block for a configuration (search_d0.cu); large_pool: K-S-L's layout
-size_t search_smem_bytes(int hbits, int kpl, int cpl, int L, int large_pool, int vc_bits);
+size_t search_smem_bytes(int hbits, int kpl, int cpl, int L, int large_pool, int vc_bits, int Dp);
 
 // K-L1: detour-ranked forward rows for new ids [first, first + n_new) from candidates [n_new][nc]
 // (reads the snapshot rows of the candidates, writes rows first..first+n_new-1; disjoint by construction)
@@ -108,13 +108,16 @@ cudaError_t launch_knn_exact(const float* vec, int dq, int64_t n, const uint32_t
                              uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
                              cudaStream_t st);
 
-// K-G on tcgen05 (TF32) + K-R exact re-rank + certificate + exact FFMA fallback (knn_tc.cu)
+// K-G on tcgen05 (TF32) + K-R exact re-rank + certificate + exact FFMA fallback (knn_tc.cu).  bound_d (nullable):
+// [nq][k] exact distances of k live rows per query (ascending; +inf padded) whose k-th bounds the true k-th from
+// above, used as the main pass's pruning threshold instead of the sample pass
 bool knn_tc_supported(int dq, int64_t q_stride, const float* Q, int k);
 size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k);
 cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
                           int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
                           uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
-                          cudaStream_t st, uint32_t* n_fallback);
+                          cudaStream_t st, uint32_t* n_fallback,
+                          const float* bound_d = nullptr);
 
 // K-M: merge G lists [G][nq][k] (ids/dists) -> first k per query by (dist, id)
 cudaError_t launch_merge_topk(const uint32_t* ids, const float* d, int G, int64_t nq, int k, uint32_t* out_ids,

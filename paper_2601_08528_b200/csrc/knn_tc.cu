@@ -647,7 +647,7 @@ size_t knn_tc_scratch_bytes(int64_t nq, int64_t n, int dq, int k) {
 static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
                           int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
                           uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
-                          cudaStream_t st, uint32_t* n_fallback, bool inner) {
+                          cudaStream_t st, uint32_t* n_fallback, bool inner, const float* bound_d) {
   if (nq <= 0) return cudaSuccess;
   // the sample pass: ~4 units per SM (C2: 5.75 vs 5.92 ms end to end at 8; 2 and 16 were no better)
   static const int inner_ups = [] {  // SVF_KNN_INNER_UPS: tuning override
@@ -675,9 +675,14 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
   float* fb_d = reinterpret_cast<float*>(sp);
   sp += al((size_t)nq * k * 4);
   float* thr0 = nullptr;
-  const int64_t S = (self_base < 0 && !inner) ? sample_rows(n, nq) : 0;
+  // the pruning bound: the caller's k live rows per query (a graph search, DESIGN §6 K-G) or the sample pass
+  const int64_t S = (self_base < 0 && !inner && bound_d == nullptr) ? sample_rows(n, nq) : 0;
   uint32_t* s_ids = nullptr;
-  float* s_d = nullptr;
+  float* s_d = const_cast<float*>(bound_d);
+  if (bound_d != nullptr) {
+    thr0 = reinterpret_cast<float*>(sp);
+    sp += al((size_t)nq * 4);
+  }
   if (S > 0) {
     thr0 = reinterpret_cast<float*>(sp);
     sp += al((size_t)nq * 4);
@@ -693,7 +698,7 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
     // k distinct live rows with their exact distances bound the true k-th from above whether or not the
     // sample's own certificate holds, so the sample pass needs neither the fallback nor a host synchronisation
     cudaError_t es = knn_tc_impl(vec, dq, S, tomb, Q, q_stride, q_dim, nq, k, metric, -1, s_ids, s_d, sp, rest,
-                                 num_sms, st, nullptr, true);
+                                 num_sms, st, nullptr, true, nullptr);
     if (es != cudaSuccess) return es;
   }
 
@@ -710,7 +715,7 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
                                                                                                    npieces, facts);
   stage_queries_kernel<<<(unsigned)((nq * (int64_t)qa_w + 255) / 256), 256, 0, st>>>(Q, q_stride, q_dim, nq, p.kc,
                                                                                        metric, qa);
-  if (S > 0)
+  if (thr0 != nullptr)
     prune_threshold_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(Q, q_stride, q_dim, nq, k, s_d, metric,
                                                                          dq * 4, facts, thr0);
   TcArgs a{nq, n, p.kc, p.stages, p.rows_per_split, p.splits, p.units, tomb, self_base, metric, cand,
@@ -767,9 +772,9 @@ static cudaError_t knn_tc_impl(const float* vec, int dq, int64_t n, const uint32
 cudaError_t launch_knn_tc(const float* vec, int dq, int64_t n, const uint32_t* tomb, const float* Q,
                           int64_t q_stride, int q_dim, int64_t nq, int k, int metric, int64_t self_base,
                           uint32_t* out_ids, float* out_d, void* scratch, size_t scratch_bytes, int num_sms,
-                          cudaStream_t st, uint32_t* n_fallback) {
+                          cudaStream_t st, uint32_t* n_fallback, const float* bound_d) {
   return knn_tc_impl(vec, dq, n, tomb, Q, q_stride, q_dim, nq, k, metric, self_base, out_ids, out_d, scratch,
-                     scratch_bytes, num_sms, st, n_fallback, false);
+                     scratch_bytes, num_sms, st, n_fallback, false, bound_d);
 }
 
 }  // namespace svf

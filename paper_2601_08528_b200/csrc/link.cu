@@ -28,28 +28,36 @@ __device__ __forceinline__ int map_find(const uint32_t* mid, const uint16_t* mpo
 // count(i) = |{ j < i : C[i] in row(C[j]) }| ("detourable paths"); stable sort by (count, i) (I11);
 // select the first min(R, m): prefix [0,P) in detour order, tail [P,R) sorted by key(d, id) (I12).
 // Rows are read from `graph` (the snapshot) and written to out_ids/out_d row b (disjoint from every row read).
+//
+// No sorting network (DESIGN.md §6 K-L1): the rank of i in (count, i) order is the number of entries with a smaller
+// count (exclusive prefix of a count histogram) plus the entries with the same count and a smaller i (match_any
+// peers in 32-wide chunks, in i order); and because C is in key order, the tail -- the selected entries past the
+// prefix, sorted by key -- is simply those entries in i order (a ballot prefix).  A C that is not in key order (an
+// svf_link_candidates caller's) falls back to a warp sort of the tail.
 template <int E>
 __global__ void __launch_bounds__(kLinkWarps * 32)
     detour_select_kernel(const uint32_t* __restrict__ graph, uint32_t* __restrict__ out_ids,
                          float* __restrict__ out_d, int R, int P, int64_t n_new,
                          const uint32_t* __restrict__ cand_ids, const float* __restrict__ cand_d, int nc, int mbits) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NC = 32 * E;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int M = 1 << mbits;
-  const size_t per_warp = (size_t)nc * 4 + (size_t)nc * 4 + (size_t)M * 4 + (size_t)M * 2 + 16 + 512;
+  const size_t per_warp = (size_t)NC * 4 * 4 + (size_t)M * 6 + 64;
   unsigned char* base = smem + ((per_warp + 15) & ~(size_t)15) * wib;
-  uint32_t* bloom = reinterpret_cast<uint32_t*>(base);  // 4096-bit membership filter of C (quick reject)
-  uint32_t* sC = bloom + 128;
-  uint32_t* cnt = sC + nc;
-  uint32_t* mid = cnt + nc;
+  uint32_t* sC = reinterpret_cast<uint32_t*>(base);
+  uint32_t* cnt = sC + NC;
+  uint32_t* hist = cnt + NC;   // count histogram -> exclusive prefix
+  uint32_t* run = hist + NC;   // entries of each count already ranked
+  uint32_t* mid = run + NC;
   uint16_t* mpos = reinterpret_cast<uint16_t*>(mid + M);
   const int64_t b = (int64_t)blockIdx.x * kLinkWarps + wib;
   if (b >= n_new) return;
   const uint32_t* C = cand_ids + b * nc;
   const float* Cd = cand_d + b * nc;
+  const unsigned lt = (1u << lane) - 1u;
 
   for (int i = lane; i < M; i += 32) mid[i] = kSent;
-  for (int i = lane; i < 128; i += 32) bloom[i] = 0u;
   int m = nc;
   for (int i0 = 0; i0 < nc; i0 += 32) {
     const int i = i0 + lane;
@@ -61,47 +69,91 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     }
   }
   __syncwarp();
-  for (int i = lane; i < m; i += 32) {
-    const uint32_t c = C[i];
-    sC[i] = c;
+  // stage C (id -> position map) and check it is in key order
+  bool sorted = true;
+  for (int i = lane; i < NC; i += 32) {
     cnt[i] = 0;
-    uint32_t h = (c * 0x9E3779B1u) >> (32 - mbits);
-    while (atomicCAS(mid + h, kSent, c) != kSent) h = (h + 1) & (uint32_t)(M - 1);
-    mpos[h] = (uint16_t)i;
-    const uint32_t fb = (c * 0x85EBCA6Bu) >> 20;
-    atomicOr(bloom + (fb >> 5), 1u << (fb & 31));
-  }
-  __syncwarp();
-  // detour counts over the snapshot rows of C[0..m-1]: 16 coalesced row slices in flight per lane
-  const int total = m * R;
-  const int rshift = (R & (R - 1)) == 0 ? __ffs(R) - 1 : -1;
-  constexpr int UF = 16;
-  for (int f0 = 0; f0 < total; f0 += 32 * UF) {
-    uint32_t u[UF];
-    int jj[UF];
-#pragma unroll
-    for (int t = 0; t < UF; ++t) {
-      const int f = f0 + t * 32 + lane;
-      jj[t] = rshift >= 0 ? (f >> rshift) : f / R;
-      u[t] = f < total ? __ldg(graph + (size_t)sC[jj[t]] * R + (f - jj[t] * R)) : kSent;
-    }
-#pragma unroll
-    for (int t = 0; t < UF; ++t) {
-      const uint32_t fb = (u[t] * 0x85EBCA6Bu) >> 20;
-      if (u[t] != kSent && ((bloom[fb >> 5] >> (fb & 31)) & 1u)) {
-        const int i = map_find(mid, mpos, mbits, u[t]);
-        if (i > jj[t]) atomicAdd(cnt + i, 1u);
+    hist[i] = 0;
+    run[i] = 0;
+    if (i < m) {
+      const uint32_t c = C[i];
+      sC[i] = c;
+      uint32_t h = (c * 0x9E3779B1u) >> (32 - mbits);
+      while (atomicCAS(mid + h, kSent, c) != kSent) h = (h + 1) & (uint32_t)(M - 1);
+      mpos[h] = (uint16_t)i;
+      if (i > 0) {
+        const float d0 = Cd[i - 1], d1 = Cd[i];
+        sorted = sorted && (d0 < d1 || (d0 == d1 && C[i - 1] < c));
       }
     }
   }
+  sorted = __all_sync(0xffffffffu, sorted);
   __syncwarp();
-  uint64_t key[E];
+  // detour counts over the snapshot rows of C[0..m-2] (row m-1 can only precede nothing): JU rows in flight
+  constexpr int JU = 8;
+  const int nrow = m - 1;
+  for (int j0 = 0; j0 < nrow; j0 += JU) {
+    uint32_t u[JU][2];
+#pragma unroll
+    for (int t = 0; t < JU; ++t) {
+      const int j = j0 + t;
+      const uint32_t* row = graph + (size_t)(j < nrow ? sC[j] : 0) * R;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = h * 32 + lane;
+        u[t][h] = (j < nrow && s < R) ? __ldg(row + s) : kSent;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < JU; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t x = u[t][h];
+        if (x == kSent) continue;
+        const int i = map_find(mid, mpos, mbits, x);
+        if (i > j0 + t) atomicAdd(cnt + i, 1u);
+      }
+    // rows longer than 64 slots (R <= 128): the rest of each row
+    for (int s0 = 64; s0 < R; s0 += 32)
+      for (int t = 0; t < JU && j0 + t < nrow; ++t) {
+        const int s = s0 + lane;
+        const uint32_t x = s < R ? __ldg(graph + (size_t)sC[j0 + t] * R + s) : kSent;
+        if (x == kSent) continue;
+        const int i = map_find(mid, mpos, mbits, x);
+        if (i > j0 + t) atomicAdd(cnt + i, 1u);
+      }
+  }
+  __syncwarp();
+  // rank in (count, i) order
+  for (int i = lane; i < m; i += 32) atomicAdd(hist + cnt[i], 1u);
+  __syncwarp();
+  {
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < NC; c0 += 32) {  // exclusive prefix of the histogram
+      const uint32_t hv = hist[c0 + lane];
+      uint32_t x = hv;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      hist[c0 + lane] = carry + x - hv;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncwarp();
+  uint32_t rank[E];
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int i = r * 32 + lane;
-    key[r] = i < m ? (((uint64_t)cnt[i] << 32) | (uint32_t)i) : kEmptyKey;
+    const uint32_t ci = i < m ? cnt[i] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, ci);
+    rank[r] = 0xFFFFFFFFu;
+    if (i < m) rank[r] = hist[ci] + run[ci] + __popc(peers & lt);
+    __syncwarp();
+    if (i < m && (peers & lt) == 0u) run[ci] += __popc(peers);  // the group's lowest lane
+    __syncwarp();
   }
-  warp_sort<E>(key, lane);  // (count, i) ascending == stable sort by count
   const int sel = min(R, m);
   const int npre = min(P, sel);
   uint32_t* row = out_ids + (size_t)b * R;
@@ -111,37 +163,59 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     rowd[s] = __int_as_float(0x7F800000);
   }
   __syncwarp();
-  // prefix: detour order; remaining selected entries staged (as (d,id) keys) for the tail sort
-  uint64_t* tkeys = reinterpret_cast<uint64_t*>(mid);  // reuse the map storage (M*4 >= 2*nc*... >= 8*R)
-  __syncwarp();
+  // prefix: detour order
 #pragma unroll
   for (int r = 0; r < E; ++r) {
-    const int e = r * 32 + lane;
-    if (e < sel) {
-      const int i = (int)(uint32_t)key[r];
-      if (e < npre) {
-        row[e] = sC[i];
-        rowd[e] = Cd[i];
-      } else {
-        tkeys[e - npre] = make_key(Cd[i], sC[i]);
-      }
+    const int i = r * 32 + lane;
+    if (i < m && rank[r] < (uint32_t)npre) {
+      row[rank[r]] = sC[i];
+      rowd[rank[r]] = Cd[i];
     }
   }
-  __syncwarp();
-  const int ntail = sel - npre;
-  uint64_t tk[4];
+  if (sorted) {
+    // tail: the selected entries past the prefix, in i (= key) order
+    int running = 0;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int e = r * 32 + lane;
-    tk[r] = e < ntail ? tkeys[e] : kEmptyKey;
-  }
-  warp_sort<4>(tk, lane);
+    for (int r = 0; r < E; ++r) {
+      const int i = r * 32 + lane;
+      const bool tail = i < m && rank[r] >= (uint32_t)npre && rank[r] < (uint32_t)sel;
+      const unsigned tm = __ballot_sync(0xffffffffu, tail);
+      if (tail) {
+        const int pos = P + running + __popc(tm & lt);
+        row[pos] = sC[i];
+        rowd[pos] = Cd[i];
+      }
+      running += __popc(tm);
+    }
+  } else {
+    uint64_t tk[4];  // R - P <= 128
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int e = r * 32 + lane;
-    if (e < ntail) {
-      row[P + e] = key_id(tk[r]);
-      rowd[P + e] = key_dist(tk[r]);
+    for (int r = 0; r < 4; ++r) tk[r] = kEmptyKey;
+    int running = 0;
+    uint64_t* tkeys = reinterpret_cast<uint64_t*>(hist);  // hist + run: 2 * NC u32 = NC keys >= R - P
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int i = r * 32 + lane;
+      const bool tail = i < m && rank[r] >= (uint32_t)npre && rank[r] < (uint32_t)sel;
+      const unsigned tm = __ballot_sync(0xffffffffu, tail);
+      if (tail) tkeys[running + __popc(tm & lt)] = make_key(Cd[i], sC[i]);
+      running += __popc(tm);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = r * 32 + lane;
+      tk[r] = e < running ? tkeys[e] : kEmptyKey;
+    }
+    warp_sort<4>(tk, lane);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = r * 32 + lane;
+      if (e < running) {
+        row[P + e] = key_id(tk[r]);
+        rowd[P + e] = key_dist(tk[r]);
+      }
     }
   }
 }
@@ -249,9 +323,9 @@ template <int E>
 cudaError_t launch_detour_e(const uint32_t* graph, uint32_t* out_ids, float* out_d, int R, int P, int64_t n_new,
                             const uint32_t* cand_ids, const float* cand_d, int nc, cudaStream_t st) {
   int mbits = 1;
-  while ((1 << mbits) < 2 * nc || (1 << mbits) < 256) ++mbits;  // >= 2x load factor, room for 128 tail keys
+  while ((1 << mbits) < 4 * nc) ++mbits;  // id -> position map at load <= 1/4 (misses end at the first probe)
   const int M = 1 << mbits;
-  const size_t per_warp = (((size_t)nc * 8 + (size_t)M * 6 + 16 + 512) + 15) & ~(size_t)15;
+  const size_t per_warp = (((size_t)32 * E * 16 + (size_t)M * 6 + 64) + 15) & ~(size_t)15;
   const size_t smem = per_warp * kLinkWarps;
   auto kern = detour_select_kernel<E>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -229,11 +229,17 @@ __device__ __forceinline__ void merge_all(const SearchArgs& a, uint64_t (&pool)[
 // Shared memory: one region per warp, [visited table 2^hbits | parents 8 | query id | survivor ids MP | keys 2xMP |
 // counts].  A query served by W warps uses the first warp's table and query id and every warp's own parents,
 // ids, keys and counts, so one-warp and two-warp (pair) processing share the layout.
+// SVF_KS_TMA_ROW = 1: the one-warp kernel stages the speculative next parent's neighbour row in shared memory with a
+// 1-D bulk copy (TMA unit, mbarrier completion) instead of holding it in registers (north star: "neighbour lists ...
+// staged in shared memory via TMA"; A/B in DESIGN §6 K-S).  The tail then also holds [row buffer MP u32 | mbarrier].
+#ifndef SVF_KS_TMA_ROW
+#define SVF_KS_TMA_ROW 0
+#endif
 template <int CPL>
 struct Smem {
   static constexpr int MP = 32 * CPL;
   static size_t __host__ __device__ head_bytes(int hbits) { return ((size_t)4 << hbits) + 32 + 16; }
-  static constexpr size_t tail_bytes = (size_t)MP * 4 + (size_t)2 * MP * 8 + 16;
+  static constexpr size_t tail_bytes = (size_t)MP * 4 + (size_t)2 * MP * 8 + 16 + (SVF_KS_TMA_ROW ? (size_t)MP * 4 + 16 : 0);
   static size_t __host__ __device__ warp_bytes(int hbits) { return (head_bytes(hbits) + tail_bytes + 15) & ~(size_t)15; }
   static size_t __host__ __device__ block_bytes(int hbits) { return kSearchWarpsPerBlock * warp_bytes(hbits); }
 };
@@ -288,6 +294,22 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
   };
   auto cnts_of = [&](int w) {
     return reinterpret_cast<int*>(wbase[w] + SM::head_bytes(a.hbits) + (size_t)MP * 4 + (size_t)2 * MP * 8);
+  };
+  constexpr bool TMA_ROW = SVF_KS_TMA_ROW && W == 1;
+  uint32_t* rowbuf = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnts_of(h)) + 16);
+  uint64_t* rowbar = reinterpret_cast<uint64_t*>(rowbuf + MP);
+  uint32_t rphase = 0;
+  bool rpending = false;  // a bulk copy into rowbuf may still be landing
+  if (TMA_ROW) {
+    if (lane == 0) bulk_mbar_init(rowbar);
+    __syncwarp();
+  }
+  auto row_settle = [&]() {  // wait for the outstanding bulk copy (before reading or re-filling rowbuf, or leaving)
+    if (TMA_ROW && rpending) {
+      bulk_wait(rowbar, rphase);
+      rphase ^= 1u;
+      rpending = false;
+    }
   };
   constexpr int WPQ = W;
   const bool resume = WPQ == 2 && a.is_tail;          // chained kernel: continue suspended queries
@@ -464,6 +486,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         if (lane == 0) ho_ex = *reinterpret_cast<volatile unsigned long long*>(a.ho + 3);  // used next iteration
       }
       if (a.max_iter > 0 && (int)iters == a.max_iter) break;
+      __syncwarp();  // the previous iteration's reads of spar are done before it is rewritten
       int np = 0;
 #pragma unroll
       for (int r = 0; r < KPL; ++r) {
@@ -497,7 +520,6 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
       // registers when the guess was right
       uint32_t rowv[CPL];
       const bool hit = np == 1 && spar[0] == spec_id;
-#pragma unroll
       for (int r = 0; r < CPL; ++r) {
         const int e = r * 32 + lane;
         rowv[r] = kSent;
@@ -513,10 +535,17 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
       if (nxt != kEmptyKey) {
         if (a.p == 1) {
           spec_id = key_id(nxt);
+          if (TMA_ROW) {
+            row_settle();
+            __syncwarp();  // every lane's reads of rowbuf are done
+            if (lane == 0) bulk_copy_g2s(rowbuf, a.graph + (size_t)spec_id * a.R, (uint32_t)a.R * 4u, rowbar);
+            rpending = true;
+          } else {
 #pragma unroll
-          for (int r = 0; r < CPL; ++r) {
-            const int e = r * 32 + lane;
-            if ((r % WPQ) == h) spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
+            for (int r = 0; r < CPL; ++r) {
+              const int e = r * 32 + lane;
+              if ((r % WPQ) == h) spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
+            }
           }
         } else if (h == 0 && lane < ((a.R * 4 + 127) >> 7)) {
           const uint32_t* prow = a.graph + (size_t)key_id(nxt) * a.R + lane * 32;
@@ -579,6 +608,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
     }
     __syncwarp();
   }
+  row_settle();  // no bulk copy outlives the warp (its block's shared memory may be released)
 }
 
 template <int KPL, int CPL, int DQT, int WPQ>

@@ -24,11 +24,14 @@ namespace svf {
 
 namespace {
 
-// per-warp shared memory: [visited cache 2^hbits entries (u16 tags or u32 ids) | pool Lp u64 | survivor ids MP u32 |
-// keys MP u64 | new keys MP u64 | (spare) MP u32 | query slot 2 u64 | parents 8 u32]
+// per-warp shared memory: [query Dp f32 | visited cache 2^hbits entries (u16 tags or u32 ids) | pool Lp u64 |
+// survivor ids MP u32 | keys MP u64 | new keys MP u64 | (spare) MP u32 | query slot 2 u64 | parents 8 u32]
 struct LpLayout {
-  int hbits, Lp, MP, c16;
-  __host__ __device__ size_t pool_off() const { return (((size_t)(c16 ? 2 : 4) << hbits) + 15) & ~(size_t)15; }
+  int hbits, Lp, MP, c16, Dp;
+  __host__ __device__ size_t cache_off() const { return ((size_t)Dp * 4 + 15) & ~(size_t)15; }
+  __host__ __device__ size_t pool_off() const {
+    return cache_off() + ((((size_t)(c16 ? 2 : 4) << hbits) + 15) & ~(size_t)15);
+  }
   __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
   __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
   __host__ __device__ size_t ck_off() const { return skey_off() + (size_t)MP * 8; }
@@ -40,9 +43,100 @@ struct LpLayout {
 #ifndef SVF_MINB_LP
 #define SVF_MINB_LP 7
 #endif
+
+// Gather geometry of K-S-L: at most 8 lanes per row (teams of T lanes, NV float4 per lane) and U rows per team per
+// round, U as large as SVF_LP_XREGS (48) registers of row data allow -- the query lives in shared memory, not in registers, so the
+// registers go to rows in flight: D = 96: 4 x 4 = 16 rows per round, D = 128: 4 x 3 = 12, D = 200: 4 x 1 = 4.
+#ifndef SVF_LP_XREGS
+#define SVF_LP_XREGS 48
+#endif
+// SVF_LP_QSMEM = 1: the gather reads the query from shared memory (gather_keys_lp) and spends the registers on rows
+// in flight; 0 (default): the query fragment stays in registers and the gather is K-S's (U = SVF_GATHER_U_LP rows
+// per team per round).  Measured (profiles/r02_lp_variants.md): at 7 blocks/SM the register query is faster at D =
+// 128 (itopk 128, 4096 queries: 1.33 vs 1.41 ms) and equal at D = 200.
+#ifndef SVF_LP_QSMEM
+#define SVF_LP_QSMEM 0
+#endif
 #ifndef SVF_GATHER_U_LP
 #define SVF_GATHER_U_LP 2
 #endif
+// SVF_LP_EARLY_ROW = 1: after each merge the exact next parent's row is loaded at once when the speculation missed
+#ifndef SVF_LP_EARLY_ROW
+#define SVF_LP_EARLY_ROW 1
+#endif
+// SVF_LP_ONE_WRITER = 1: one writer per cache slot per round (match_any) and a warp barrier between the round's cache
+// reads and writes, so compute-sanitizer's racecheck sees no shared-memory hazard; 0: plain stores (the lossy cache
+// tolerates the benign write/write and read/write races: any value a slot holds is a valid visited tag or empty)
+#ifndef SVF_LP_ONE_WRITER
+#define SVF_LP_ONE_WRITER 1
+#endif
+template <int DQT>
+struct GeoLP {
+  static constexpr int T = DQT <= 4 ? 1 : DQT <= 8 ? 2 : DQT <= 16 ? 4 : 8;
+  static constexpr int NV = DQT ? (DQT + T - 1) / T : 1;
+  static constexpr int U0 = SVF_LP_XREGS / (4 * NV);
+  static constexpr int U = U0 < 1 ? 1 : (U0 > 4 ? 4 : U0);
+};
+
+// Distances of the S ids sid[0..S) -> keys skey[0..S), the query read from shared memory (qs, Dp floats).
+// DQT > 0: compile-time geometry (GeoLP); DQT = 0: the runtime team of SearchArgs (team * nv >= dq, nv <= 4), U = 2.
+template <int DQT>
+__device__ __forceinline__ void gather_keys_lp(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
+                                               const float4* qs, int lane) {
+  constexpr int NVC = DQT ? GeoLP<DQT>::NV : 4;
+  constexpr int U = DQT ? GeoLP<DQT>::U : 2;
+  const int T = DQT ? GeoLP<DQT>::T : a.team, NV = DQT ? GeoLP<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
+  const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
+  const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
+  __syncwarp();
+  // rows beyond the first round: pull their lines toward L2 now (no registers), so later rounds hit L2
+  for (int i = nteams * U * 4 + lane; i < S * 4; i += 32) {
+    const char* p = reinterpret_cast<const char*>(vec4 + (size_t)sid[i >> 2] * DQ) + (i & 3) * 128;
+    if ((i & 3) * 128 < DQ * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+  for (int base = 0; base < S; base += nteams * U) {
+    float4 xv[U][NVC];
+    uint32_t id[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int s = base + team + nteams * u;
+      id[u] = s < S ? sid[s] : kSent;
+      const float4* row = vec4 + (size_t)(id[u] == kSent ? 0 : id[u]) * DQ;
+#pragma unroll
+      for (int v = 0; v < NVC; ++v) {
+        const int c = tl + T * v;
+        xv[u][v] = (v < NV && c < DQ && id[u] != kSent) ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc = 0.f;
+#pragma unroll
+      for (int v = 0; v < NVC; ++v) {
+        const int c = tl + T * v;
+        if (v < NV && c < DQ) {
+          const float4 q = qs[c];
+          if (a.metric == 0) {
+            const float dx = xv[u][v].x - q.x, dy = xv[u][v].y - q.y, dz = xv[u][v].z - q.z, dw = xv[u][v].w - q.w;
+            acc = fmaf(dx, dx, acc);
+            acc = fmaf(dy, dy, acc);
+            acc = fmaf(dz, dz, acc);
+            acc = fmaf(dw, dw, acc);
+          } else {
+            acc = fmaf(xv[u][v].x, q.x, acc);
+            acc = fmaf(xv[u][v].y, q.y, acc);
+            acc = fmaf(xv[u][v].z, q.z, acc);
+            acc = fmaf(xv[u][v].w, q.w, acc);
+          }
+        }
+      }
+      for (int off = T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      const int s = base + team + nteams * u;
+      if (tl == 0 && s < S) skey[s] = make_key((a.metric == 0 ? acc : -acc) + 0.0f, id[u]);  // canonical +0
+    }
+  }
+  __syncwarp();
+}
 
 // Visited cache slot and tag of an id.  vc_bits = B > 0: ids are < 2^B and h = id * odd mod 2^B is a bijection of
 // [0, 2^B); the slot is h's top hbits and the tag its low B - hbits bits (+1, so 0 marks an empty slot), stored in 16
@@ -76,10 +170,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   constexpr int MP = 32 * CPL;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int VB = a.vc_bits;  // 16-bit tagged cache when > 0
-  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP, VB > 0};
+  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP, VB > 0, a.dq * 4};
   unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
-  uint32_t* cache = reinterpret_cast<uint32_t*>(base);
-  uint16_t* cache16 = reinterpret_cast<uint16_t*>(base);
+  float4* qs = reinterpret_cast<float4*>(base);
+  uint32_t* cache = reinterpret_cast<uint32_t*>(base + lay.cache_off());
+  uint16_t* cache16 = reinterpret_cast<uint16_t*>(base + lay.cache_off());
   uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());
   uint32_t* sid = reinterpret_cast<uint32_t*>(base + lay.sid_off());
   uint64_t* skey = reinterpret_cast<uint64_t*>(base + lay.skey_off());
@@ -88,10 +183,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   unsigned long long* qslot = reinterpret_cast<unsigned long long*>(base + lay.misc_off());
   uint32_t* spar = reinterpret_cast<uint32_t*>(base + lay.misc_off() + 16);
   const int H = 1 << a.hbits;
-  const int T = DQT ? Geo<DQT>::T : a.team;
-  const int tl = lane & (T - 1);
   const int L = a.L;
-  constexpr int U = DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U;
 
   for (;;) {
     if (lane == 0) {
@@ -116,20 +208,22 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     unsigned long long t_start = 0;
     if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    // S0: stage the query through the cache region (coalesced; the host keeps it >= Dp floats), keep this lane's
-    // fragment, clear the cache
+    // S0: the query row into this warp's shared memory (coalesced, zero-padded to Dp), the visited cache cleared
     const float* qg = a.Q + (size_t)qi * a.q_stride;
-    float* qstage = reinterpret_cast<float*>(cache);
-    for (int i = lane; i < a.dq * 4; i += 32) qstage[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
+    float* qf32 = reinterpret_cast<float*>(qs);
+    for (int i = lane; i < a.dq * 4; i += 32) qf32[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
+#if !SVF_LP_QSMEM
     __syncwarp();
     float4 qv[4];
+    {
+      const int T = DQT ? Geo<DQT>::T : a.team, tl = lane & (T - 1);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int c = tl + T * v;
-      qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? reinterpret_cast<const float4*>(qstage)[c]
-                                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int v = 0; v < 4; ++v) {
+        const int c = tl + T * v;
+        qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? qs[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
-    __syncwarp();
+#endif
     if (VB) {
       for (int i = lane; i < (H >> 1); i += 32) cache[i] = 0u;
     } else {
@@ -137,6 +231,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     }
     __syncwarp();
 
+#if SVF_LP_QSMEM
+#define GATHER_LP(S_) gather_keys_lp<DQT>(a, sid, skey, (S_), qs, lane)
+#else
+#define GATHER_LP(S_) gather_keys<DQT, (DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U)>(a, sid, skey, (S_), qv, lane)
+#endif
     int np = 0;  // entries in the pool (<= L)
     int fu = 0;  // every entry before fu is parented
     uint32_t n_dist = 0, iters = 0, n_exp = 0;
@@ -222,18 +321,25 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           const unsigned m = __ballot_sync(0xffffffffu, ok);
           const int pos = running + __popc(m & ((1u << lane) - 1u));
           const bool keep = ok && taken + pos < a.n_init;
+          uint32_t slot = 0, tag = 0;
           if (keep) {
             sid[pos] = id;
-            uint32_t slot, tag;
             cache_pos(id, a.hbits, VB, slot, tag);
+          }
+          // one writer per slot (the lowest lane), so the cache never sees two stores to one slot at once
+          const unsigned peers = SVF_LP_ONE_WRITER
+                                     ? __match_any_sync(0xffffffffu, keep ? slot : (0x80000000u | (uint32_t)lane))
+                                     : 0u;
+          if (keep && (peers & ((1u << lane) - 1u)) == 0u) {
             if (VB) cache16[slot] = (uint16_t)tag;
             else cache[slot] = tag;
           }
+          if (SVF_LP_ONE_WRITER) __syncwarp();
           running += __popc(m);
         }
         const int kept = min(running, a.n_init - taken);
         taken += kept;
-        gather_keys<DQT, U>(a, sid, skey, kept, qv, lane);
+        GATHER_LP(kept);
         n_dist += kept;
         update(kept);
       }
@@ -256,6 +362,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
 #endif
     for (;;) {
       if (a.max_iter > 0 && (int)iters == a.max_iter) break;
+      __syncwarp();  // the previous iteration's reads of spar are done before it is rewritten
       // S2 GetNearest: scan from the cursor, mark the first p unparented entries
       int npar = 0, last = -1;
       for (int s0 = fu; s0 < np && npar < a.p; s0 += 32) {
@@ -332,20 +439,39 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           ok = VB ? cache16[slot] != (uint16_t)tag : cache[slot] != tag;
         }
         const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (ok) {
-          sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+        if (ok) sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+        if (SVF_LP_ONE_WRITER) __syncwarp();  // every lane's cache read of this round before any write
+        // one writer per slot (the lowest lane); ids colliding in a slot are all scored, the cache keeps one
+        const unsigned peers = SVF_LP_ONE_WRITER
+                                   ? __match_any_sync(0xffffffffu, ok ? slot : (0x80000000u | (uint32_t)lane))
+                                   : 0u;
+        if (ok && (peers & ((1u << lane) - 1u)) == 0u) {
           if (VB) cache16[slot] = (uint16_t)tag;
           else cache[slot] = tag;
         }
+        if (SVF_LP_ONE_WRITER) __syncwarp();
         running += __popc(m);
       }
       SVF_LPH(2)
       if (running == 0) continue;
       // S5 distances, S6 merge
-      gather_keys<DQT, U>(a, sid, skey, running, qv, lane);
+      GATHER_LP(running);
       n_dist += running;
       SVF_LPH(3)
       update(running);
+      // p = 1: the next parent is now known exactly (pool[fu] is unparented whenever fu < np); if the speculative
+      // row is not its row, load the right one at once, so the fetch overlaps the next select
+      if (SVF_LP_EARLY_ROW && a.p == 1 && fu < np) {
+        const uint32_t nid = key_id(pool[fu]);
+        if (nid != spec_id) {
+          spec_id = nid;
+#pragma unroll
+          for (int r = 0; r < CPL; ++r) {
+            const int e = r * 32 + lane;
+            spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)nid * a.R + e) : kSent;
+          }
+        }
+      }
       SVF_LPH(4)
     }
 
@@ -383,14 +509,14 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
 
 }  // namespace
 
-static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl, int c16) {
-  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl, c16}.warp_bytes();
+static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl, int c16, int Dp) {
+  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl, c16, Dp}.warp_bytes();
 }
 
 template <int CPL, int DQT>
 static cudaError_t launch_lp_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   auto kern = search_lp_kernel<CPL, DQT>;
-  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL, a.vc_bits > 0);
+  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL, a.vc_bits > 0, a.dq * 4);
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0, cached_dev = -1;
   int dev = 0, per_sm = 0;

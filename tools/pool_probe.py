@@ -25,13 +25,23 @@ def main():
     ap.add_argument("--itopks", default="128,192,256")
     ap.add_argument("--batches", default="4096,10000")
     ap.add_argument("--width", type=int, default=1)
+    ap.add_argument("--n", type=int, default=0, help="base rows (0 = the config's)")
+    ap.add_argument("--degree", type=int, default=64)
+    ap.add_argument("--no-insert", action="store_true")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    X = base_rows(a.config)
+    from workloads import config_spec
+
+    X = base_rows(a.config, 0, a.n or None)
     n = len(X)
-    idx = svf.Index.build(torch.from_numpy(X).to(dev), degree=64, capacity=n + 40_000, build_itopk=a.build_itopk)
+    idx = svf.Index.build(torch.from_numpy(X).to(dev), degree=a.degree, capacity=n + 40_000, build_itopk=a.build_itopk,
+                          metric=config_spec(a.config)["metric"])
     Qn = torch.from_numpy(base_rows(a.config, n, 20_000)).to(dev)
+    if a.config == "C4":   # C4's queries come from another modality (OOD): probe with those
+        from workloads import query_rows
+
+        Qn = torch.from_numpy(query_rows("C4", 20_000)).to(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     res = {"config": f"{a.config} graph at L_build {a.build_itopk}; queries = fresh insert vectors", "runs": []}
     idx.set_search_handoff(0)
@@ -65,6 +75,10 @@ def main():
                                         / 6545e9, 4)
             print(json.dumps(row), flush=True)
             res["runs"].append(row)
+    if a.no_insert:
+        if a.out:
+            json.dump(res, open(a.out, "w"), indent=1)
+        return
     idx.set_search_handoff(-1)
     idx.set_search_params(1, 0, 0, 0)
     idx.profile(True)
