@@ -28,6 +28,38 @@ __device__ __forceinline__ float key_dist(uint64_t k) {
   return k == kEmptyKey ? __int_as_float(0x7F800000) : ord2f((uint32_t)(k >> 32));
 }
 
+// ---- packed fp32 pairs (sm_100 FADD2 / FFMA2: two fp32 operations per issue slot) -------------------------------
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f2sum(uint64_t r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return a + b;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// acc += (x - q)^2 (metric 0, squared L2) or x * q (metric 1, inner product) over one float4, as two packed pairs:
+// the low half accumulates components x, z and the high half y, w; f2sum(acc) is the lane's partial sum
+__device__ __forceinline__ uint64_t dist_acc4(uint64_t acc, const float4& x, const float4& q, int metric) {
+  const uint64_t x01 = f2pack(x.x, x.y), x23 = f2pack(x.z, x.w), q01 = f2pack(q.x, q.y), q23 = f2pack(q.z, q.w);
+  if (metric == 0) {
+    const uint64_t d01 = f2sub(x01, q01), d23 = f2sub(x23, q23);
+    return f2fma(d23, d23, f2fma(d01, d01, acc));
+  }
+  return f2fma(x23, q23, f2fma(x01, q01, acc));
+}
+
 __device__ __forceinline__ bool tomb_dead(const uint32_t* __restrict__ tomb, uint32_t id) {
   return tomb != nullptr && ((__ldg(tomb + (id >> 5)) >> (id & 31)) & 1u);
 }

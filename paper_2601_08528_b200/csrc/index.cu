@@ -15,7 +15,7 @@ using namespace svf;
 
 struct svf_index {
   svf_params p{};
-  int dev = 0, num_sms = 148, smem_optin = 227 * 1024;
+  int dev = 0, num_sms = 148, smem_optin = 227 * 1024, smem_sm = 228 * 1024;
   int D = 0, Dp = 0, dq = 0, R = 0, P = 0;
   int64_t cap = 0, n_alloc = 0, n_deleted = 0;
   float* vec = nullptr;
@@ -152,7 +152,8 @@ int pow2_at_least(int x) {
 }
 
 struct SearchCfg {
-  int kpl, cpl, hbits, team, nv, n_init, wpq, lp, vc_bits;
+  int kpl, cpl, hbits, team, nv, n_init, wpq, lp, vc_bits, vc_slots;
+  uint32_t vc_tmask;
 };
 
 // K-S-L (shared-memory pool kernel) for pools of more than 64 keys; SVF_LP=0 keeps the register-pool kernel (A/B)
@@ -171,13 +172,30 @@ bool lp_u32_cache() {
   }();
   return on;
 }
-// default K-S-L visited-cache size (2^bits direct-mapped slots); SVF_LP_BITS overrides it for tuning
-int lp_bits_auto(int L) {
+// K-S-L visited-cache size override (2^bits direct-mapped slots) for tuning; 0 = sized by lp_cache_slots
+int lp_bits_env() {
   static const int env = [] {
     const char* v = getenv("SVF_LP_BITS");
     return v ? atoi(v) : 0;
   }();
-  return env > 0 ? env : (L <= 256 ? 11 : 12);
+  return env;
+}
+#ifndef SVF_MINB_LP
+#define SVF_MINB_LP 7
+#endif
+// Default K-S-L visited-cache slots: pools of <= 256 keys run at SVF_MINB_LP blocks/SM (their register limit), so the
+// cache gets whatever shared memory that residency leaves once the pool and buffers are placed (C2 L_insert 128: 3120
+// 16-bit slots, C4 itopk 192: 2864; a power-of-two 2048 before round 2 recomputed 1.5x the oracle's distances, and
+// 4096 cost two blocks/SM: profiles/r02_lp_cache.json); larger pools keep 4096 slots at lower residency.
+int lp_cache_slots(const svf_index* idx, int L, int cpl, bool c16) {
+  if (L > 256) return 4096;
+  // 1 KB per block is reserved by the system; blocks are allocated in 128-byte units
+  const long per_block = ((long)idx->smem_sm / SVF_MINB_LP - 1024) & ~127L;
+  const long per_warp = (per_block / kSearchWarpsPerBlock) & ~15L;
+  // all but the cache: the per-warp layout with an 8-slot cache, minus those 8 slots
+  const long fixed = (long)search_smem_bytes(8, 0, cpl, L, 1, c16 ? 1 : 0, 0, 8) / kSearchWarpsPerBlock - 8 * (c16 ? 2 : 4);
+  const long m = (per_warp - fixed) / (c16 ? 2 : 4);
+  return (int)std::max(256L, m & ~7L);
 }
 
 bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, SearchCfg& c, std::string& why) {
@@ -202,20 +220,35 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   // invariant, only room to stage the query row
   c.lp = LP > 64 && idx->wpq != 2 && lp_enabled();
   c.vc_bits = 0;
+  c.vc_slots = 0;
+  c.vc_tmask = 0;
   if (c.lp) {
-    const int lpmin = 8;
-    c.hbits = std::max(hash_bits > 0 ? hash_bits : lp_bits_auto(L), lpmin);
-    // 16-bit tagged cache entries when every id of the index fits in hbits + 15 bits (exact, DESIGN §6 K-S-L)
+    // ids are < 2^B; 16-bit tags when a slot's run of hashed ids, ceil(2^B / M), fits 15 bits (DESIGN §6 K-S-L)
     int B = 1;
     while (B < 32 && ((int64_t)1 << B) < idx->cap) ++B;
-    B = std::max(B, c.hbits);
-    c.vc_bits = (B - c.hbits <= 15 && !lp_u32_cache()) ? B : 0;
+    const int bits = hash_bits > 0 ? std::max(hash_bits, 8) : lp_bits_env();
+    auto fits16 = [&](int M) {
+      const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
+      return B <= 31 && run <= 32768 && !lp_u32_cache();
+    };
+    int M = bits > 0 ? (1 << std::min(bits, 16)) : lp_cache_slots(idx, L, c.cpl, true);
+    c.vc_bits = fits16(M) ? B : 0;
+    if (!c.vc_bits && bits == 0) M = lp_cache_slots(idx, L, c.cpl, false);
+    c.vc_slots = M;
+    if (c.vc_bits) {
+      const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
+      int tb = 0;
+      while (((uint64_t)1 << tb) < run) ++tb;
+      c.vc_tmask = (1u << tb) - 1u;
+    }
+    c.hbits = 8;
+    while ((1 << c.hbits) < M) ++c.hbits;  // reported only (svf_last_search_counters); K-S-L uses vc_slots
   } else {
     c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   }
   if (c.hbits > 15) return why = "hash_bits too large", false;
   // a configuration whose block does not fit the opt-in shared memory is refused up front (INVALID, index intact)
-  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp, c.vc_bits, idx->Dp) > (size_t)idx->smem_optin)
+  if (search_smem_bytes(c.hbits, c.kpl, c.cpl, L, c.lp, c.vc_bits, idx->Dp, c.vc_slots) > (size_t)idx->smem_optin)
     return why = "hash_bits too large: the search block's visited tables exceed the shared memory per block", false;
   c.team = pow2_at_least((idx->dq + 3) / 4);
   c.nv = (idx->dq + c.team - 1) / c.team;
@@ -362,6 +395,8 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
   a.large_pool = c.lp && a.wpq == 1;
   a.vc_bits = c.vc_bits;
+  a.vc_slots = c.vc_slots;
+  a.vc_tmask = c.vc_tmask;
   cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   unsigned long long*& hob = update_path ? idx->ho_upd : idx->ho;
@@ -442,6 +477,7 @@ svf_status alloc_index(const svf_params* p, svf_index** out) {
   idx->dev = p->device;
   cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, p->device);
   cudaDeviceGetAttribute(&idx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+  cudaDeviceGetAttribute(&idx->smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, p->device);
   idx->D = p->dim;
   idx->Dp = (p->dim + 3) / 4 * 4;
   idx->dq = idx->Dp / 4;

@@ -75,11 +75,13 @@ struct SearchArgs {
   unsigned int q_epoch;
   int q_chunk_log2;
   int large_pool;          // 1: K-S-L, the shared-memory pool kernel (search_lp.cuh; one warp per query, no handoff)
-  int vc_bits;             // K-S-L visited cache: B > 0 = 16-bit tags over ids < 2^B (B - hbits <= 15), 0 = u32 ids
+  int vc_bits;             // K-S-L visited cache: B > 0 = 16-bit tags over ids < 2^B, 0 = u32 ids
+  int vc_slots;            // K-S-L visited cache slots M (any even count >= 8; search_lp.cuh cache_pos)
+  uint32_t vc_tmask;       // K-S-L 16-bit tags: 2^tb - 1 with 2^tb >= ceil(2^vc_bits / M), tb <= 15
 };
 cudaError_t launch_search(SearchArgs a, int kpl, int cpl, int num_sms, cudaStream_t st);
 // dynamic shared memory of one search block for a configuration (search_d0.cu); large_pool: K-S-L's layout
-size_t search_smem_bytes(int hbits, int kpl, int cpl, int L, int large_pool, int vc_bits, int Dp);
+size_t search_smem_bytes(int hbits, int kpl, int cpl, int L, int large_pool, int vc_bits, int Dp, int lp_slots);
 
 // K-L1: detour-ranked forward rows for new ids [first, first + n_new) from candidates [n_new][nc]
 // (reads the snapshot rows of the candidates, writes rows first..first+n_new-1; disjoint by construction)

@@ -91,11 +91,33 @@ constexpr int gather_u() {
                   : (KPL >= 4 && DQT > 0) ? (Geo<DQT>::NV <= 3 ? 4 : 3) : SVF_GATHER_U;
 }
 
+// Pull every 128-byte line of the rows sid[first..S) toward L2 (prefetch.global.L2: no registers, nothing to wait
+// for), so the gather rounds that load them later hit L2.  A row of DQ float4 spans up to DQ*16/128 + 1 lines when
+// DQ*16 is not a multiple of 128 (D = 200: 800-byte rows start anywhere on a 32-byte sector, 7-8 lines).
+__device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4, const uint32_t* sid, int first,
+                                                 int S, int DQ, int lane) {
+  const int rb = DQ * 16;
+  const int nl = (rb & 127) ? (rb >> 7) + 2 : (rb >> 7);  // lines a row may touch (aligned rows: exactly rb/128)
+  for (int i = first * nl + lane; i < S * nl; i += 32) {
+    const int s = i / nl, j = i - s * nl;
+    const uintptr_t r0 = reinterpret_cast<uintptr_t>(vec4 + (size_t)sid[s] * DQ);
+    const uintptr_t p = (r0 & ~(uintptr_t)127) + (uintptr_t)j * 128;
+    if (p < r0 + rb) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+
 // Distances of the S ids sid[0..S) -> keys skey[0..S): teams of T lanes per vector, U vectors per team per round
 // (U * 32/T rows in flight per warp), coalesced 16-byte gathers, FFMA, xor-shuffle reduction.
-template <int DQT, int U>
+// PF (K-S-L): a key below `pf` (the best unparented pool key) makes its id the likely next parent, so the lane that
+// computed it pulls that id's neighbour row toward L2 at once; the exact row load after the merge then hits L2.
+__device__ __forceinline__ void prefetch_graph_row(const uint32_t* graph, int R, uint32_t id) {
+  const char* p = reinterpret_cast<const char*>(graph + (size_t)id * R);
+  for (int b = 0; b < R * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+}
+
+template <int DQT, int U, bool PF = false>
 __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
-                                            const float4 (&qv)[4], int lane) {
+                                            const float4 (&qv)[4], int lane, uint64_t pf = 0ull) {
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
@@ -110,10 +132,7 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vec4 + (size_t)sid[s] * DQ), "r"(DQ * 16)
                  : "memory");
 #elif SVF_PREFETCH == 1
-  for (int i = nteams * U * 4 + lane; i < S * 4; i += 32) {
-    const char* p = reinterpret_cast<const char*>(vec4 + (size_t)sid[i >> 2] * DQ) + (i & 3) * 128;
-    if ((i & 3) * 128 < DQ * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  }
+  prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
 #endif
   for (int base = 0; base < S; base += nteams * U) {
     float4 xv[U][4];
@@ -131,23 +150,11 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      float acc = 0.f;
+      constexpr int NVC = DQT ? Geo<DQT>::NV : 4;  // float4 per lane per row (the generic path pads with zeros)
+      uint64_t acc2 = 0ull;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        if (a.metric == 0) {
-          float dx = xv[u][v].x - qv[v].x, dy = xv[u][v].y - qv[v].y;
-          float dz = xv[u][v].z - qv[v].z, dw = xv[u][v].w - qv[v].w;
-          acc = fmaf(dx, dx, acc);
-          acc = fmaf(dy, dy, acc);
-          acc = fmaf(dz, dz, acc);
-          acc = fmaf(dw, dw, acc);
-        } else {
-          acc = fmaf(xv[u][v].x, qv[v].x, acc);
-          acc = fmaf(xv[u][v].y, qv[v].y, acc);
-          acc = fmaf(xv[u][v].z, qv[v].z, acc);
-          acc = fmaf(xv[u][v].w, qv[v].w, acc);
-        }
-      }
+      for (int v = 0; v < NVC; ++v) acc2 = dist_acc4(acc2, xv[u][v], qv[v], a.metric);
+      float acc = f2sum(acc2);
       if (DQT) {
 #pragma unroll
         for (int off = Geo<DQT>::T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -157,7 +164,9 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
       const int s = base + team + nteams * u;
       if (tl == 0 && s < S) {
         float d = (a.metric == 0 ? acc : -acc) + 0.0f;  // canonical +0
-        skey[s] = make_key(d, id[u]);
+        const uint64_t key = make_key(d, id[u]);
+        skey[s] = key;
+        if (PF && key < pf) prefetch_graph_row(a.graph, a.R, id[u]);
       }
     }
   }

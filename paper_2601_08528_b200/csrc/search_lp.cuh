@@ -24,19 +24,20 @@ namespace svf {
 
 namespace {
 
-// per-warp shared memory: [query Dp f32 | visited cache 2^hbits entries (u16 tags or u32 ids) | pool Lp u64 |
-// survivor ids MP u32 | keys MP u64 | new keys MP u64 | (spare) MP u32 | query slot 2 u64 | parents 8 u32]
+// per-warp shared memory: [visited cache M entries (u16 tags or u32 ids); the query row is staged here before the
+// cache is cleared | pool Lp u64 | survivor ids MP u32 | keys MP u64 (compacted in place by C.Update) | query slot
+// 2 u64 | parents 8 u32].  M need not be a power of two (slot = multiply-shift of a hashed id), so the launcher
+// sizes the cache to whatever the target residency leaves (DESIGN.md §6 K-S-L).
 struct LpLayout {
-  int hbits, Lp, MP, c16, Dp;
-  __host__ __device__ size_t cache_off() const { return ((size_t)Dp * 4 + 15) & ~(size_t)15; }
-  __host__ __device__ size_t pool_off() const {
-    return cache_off() + ((((size_t)(c16 ? 2 : 4) << hbits) + 15) & ~(size_t)15);
+  int M, Lp, MP, c16, Dp;
+  __host__ __device__ size_t cache_bytes() const {
+    const size_t cb = (size_t)M * (c16 ? 2 : 4), qb = (size_t)Dp * 4;
+    return ((cb > qb ? cb : qb) + 15) & ~(size_t)15;
   }
+  __host__ __device__ size_t pool_off() const { return cache_bytes(); }
   __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
   __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
-  __host__ __device__ size_t ck_off() const { return skey_off() + (size_t)MP * 8; }
-  __host__ __device__ size_t cb_off() const { return ck_off() + (size_t)MP * 8; }
-  __host__ __device__ size_t misc_off() const { return cb_off() + (size_t)MP * 4; }
+  __host__ __device__ size_t misc_off() const { return skey_off() + (size_t)MP * 8; }
   __host__ __device__ size_t warp_bytes() const { return (misc_off() + 48 + 15) & ~(size_t)15; }
 };
 
@@ -44,21 +45,17 @@ struct LpLayout {
 #define SVF_MINB_LP 7
 #endif
 
-// Gather geometry of K-S-L: at most 8 lanes per row (teams of T lanes, NV float4 per lane) and U rows per team per
-// round, U as large as SVF_LP_XREGS (48) registers of row data allow -- the query lives in shared memory, not in registers, so the
-// registers go to rows in flight: D = 96: 4 x 4 = 16 rows per round, D = 128: 4 x 3 = 12, D = 200: 4 x 1 = 4.
-#ifndef SVF_LP_XREGS
-#define SVF_LP_XREGS 48
-#endif
-// SVF_LP_QSMEM = 1: the gather reads the query from shared memory (gather_keys_lp) and spends the registers on rows
-// in flight; 0 (default): the query fragment stays in registers and the gather is K-S's (U = SVF_GATHER_U_LP rows
-// per team per round).  Measured (profiles/r02_lp_variants.md): at 7 blocks/SM the register query is faster at D =
-// 128 (itopk 128, 4096 queries: 1.33 vs 1.41 ms) and equal at D = 200.
-#ifndef SVF_LP_QSMEM
-#define SVF_LP_QSMEM 0
-#endif
 #ifndef SVF_GATHER_U_LP
 #define SVF_GATHER_U_LP 2
+#endif
+// SVF_LP_WHOLE = 1: whole-warp rows at D = 200 (SVF_GATHER_W_LP / 2 rows per round); measured against teams of 16
+// lanes with 2 rows each: C4 itopk 192 11.84 -> 11.00 ms; at D = 128 the 8-lane teams stay (whole-warp: 2.01 vs
+// 1.89 ms for an itopk-128 4096-query batch), profiles/r02_lp_ab.json
+#ifndef SVF_LP_WHOLE
+#define SVF_LP_WHOLE 1
+#endif
+#ifndef SVF_GATHER_W_LP
+#define SVF_GATHER_W_LP 8
 #endif
 // SVF_LP_EARLY_ROW = 1: after each merge the exact next parent's row is loaded at once when the speculation missed
 #ifndef SVF_LP_EARLY_ROW
@@ -70,85 +67,86 @@ struct LpLayout {
 #ifndef SVF_LP_ONE_WRITER
 #define SVF_LP_ONE_WRITER 1
 #endif
-template <int DQT>
-struct GeoLP {
-  static constexpr int T = DQT <= 4 ? 1 : DQT <= 8 ? 2 : DQT <= 16 ? 4 : 8;
-  static constexpr int NV = DQT ? (DQT + T - 1) / T : 1;
-  static constexpr int U0 = SVF_LP_XREGS / (4 * NV);
-  static constexpr int U = U0 < 1 ? 1 : (U0 > 4 ? 4 : U0);
-};
 
-// Distances of the S ids sid[0..S) -> keys skey[0..S), the query read from shared memory (qs, Dp floats).
-// DQT > 0: compile-time geometry (GeoLP); DQT = 0: the runtime team of SearchArgs (team * nv >= dq, nv <= 4), U = 2.
-template <int DQT>
-__device__ __forceinline__ void gather_keys_lp(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
-                                               const float4* qs, int lane) {
-  constexpr int NVC = DQT ? GeoLP<DQT>::NV : 4;
-  constexpr int U = DQT ? GeoLP<DQT>::U : 2;
-  const int T = DQT ? GeoLP<DQT>::T : a.team, NV = DQT ? GeoLP<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
-  const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
+// Whole-warp gather for K-S-L at D = 128 / 200 (DQT = 32 / 50 float4): every lane holds NV = ceil(DQT / 32) float4 of
+// each of U rows per round (the query costs NV float4 per lane instead of K-S's 4, so the registers go to rows in
+// flight: 8 rows per round at D = 128, 4 at D = 200), and the U partial sums are reduced together by a transposing
+// butterfly (at the step with offset 2^(4-j) each lane keeps half of its values and sends the other half: U - 1 + 5 -
+// log2 U shuffles for U rows instead of 5 U), after which lane l holds row (l >> (5 - log2 U)).
+template <int DQT, int U>
+__device__ __forceinline__ void gather_keys_w(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
+                                              const float4 (&qv)[4], int lane, uint64_t pf) {
+  static_assert(U == 1 || U == 2 || U == 4 || U == 8, "U must be a power of two <= 8");
+  constexpr int NV = (DQT + 31) / 32;
+  constexpr int LU = U == 1 ? 0 : U == 2 ? 1 : U == 4 ? 2 : 3;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
   __syncwarp();
-  // rows beyond the first round: pull their lines toward L2 now (no registers), so later rounds hit L2
-  for (int i = nteams * U * 4 + lane; i < S * 4; i += 32) {
-    const char* p = reinterpret_cast<const char*>(vec4 + (size_t)sid[i >> 2] * DQ) + (i & 3) * 128;
-    if ((i & 3) * 128 < DQ * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  }
-  for (int base = 0; base < S; base += nteams * U) {
-    float4 xv[U][NVC];
+  prefetch_rows_l2(vec4, sid, U, S, DQT, lane);
+  for (int base = 0; base < S; base += U) {
+    float4 xv[U][NV];
     uint32_t id[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int s = base + team + nteams * u;
+      const int s = base + u;
       id[u] = s < S ? sid[s] : kSent;
-      const float4* row = vec4 + (size_t)(id[u] == kSent ? 0 : id[u]) * DQ;
+      const float4* row = vec4 + (size_t)(id[u] == kSent ? 0 : id[u]) * DQT;
 #pragma unroll
-      for (int v = 0; v < NVC; ++v) {
-        const int c = tl + T * v;
-        xv[u][v] = (v < NV && c < DQ && id[u] != kSent) ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int v = 0; v < NV; ++v) {
+        const int c = lane + 32 * v;
+        xv[u][v] = (c < DQT && id[u] != kSent) ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    float acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint64_t acc2 = 0ull;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc2 = dist_acc4(acc2, xv[u][v], qv[v], a.metric);
+      acc[u] = f2sum(acc2);
+    }
+    // transposing butterfly: after the step with offset 16 >> j, lane l holds the partial sums of rows whose index
+    // bits (from the top) equal l's bits 4, 3, ... (U >> (j + 1) values left)
+#pragma unroll
+    for (int j = 0; j < LU; ++j) {
+      const int off = 16 >> j;
+      const bool hi = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < (U >> (j + 1)); ++i) {
+        const float send = hi ? acc[i] : acc[i + (U >> (j + 1))];
+        const float keep = hi ? acc[i + (U >> (j + 1))] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float acc = 0.f;
+    for (int off = 16 >> LU; off > 0; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+    const int r = lane >> (5 - LU), s = base + r;
+    if ((lane & ((32 >> LU) - 1)) == 0 && s < S) {
+      uint32_t idr = id[0];
 #pragma unroll
-      for (int v = 0; v < NVC; ++v) {
-        const int c = tl + T * v;
-        if (v < NV && c < DQ) {
-          const float4 q = qs[c];
-          if (a.metric == 0) {
-            const float dx = xv[u][v].x - q.x, dy = xv[u][v].y - q.y, dz = xv[u][v].z - q.z, dw = xv[u][v].w - q.w;
-            acc = fmaf(dx, dx, acc);
-            acc = fmaf(dy, dy, acc);
-            acc = fmaf(dz, dz, acc);
-            acc = fmaf(dw, dw, acc);
-          } else {
-            acc = fmaf(xv[u][v].x, q.x, acc);
-            acc = fmaf(xv[u][v].y, q.y, acc);
-            acc = fmaf(xv[u][v].z, q.z, acc);
-            acc = fmaf(xv[u][v].w, q.w, acc);
-          }
-        }
-      }
-      for (int off = T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      const int s = base + team + nteams * u;
-      if (tl == 0 && s < S) skey[s] = make_key((a.metric == 0 ? acc : -acc) + 0.0f, id[u]);  // canonical +0
+      for (int u = 1; u < U; ++u)
+        if (r == u) idr = id[u];
+      const uint64_t key = make_key((a.metric == 0 ? acc[0] : -acc[0]) + 0.0f, idr);  // canonical +0
+      skey[s] = key;
+      if (key < pf) prefetch_graph_row(a.graph, a.R, idr);  // the likely next parent (gather_keys' PF)
     }
   }
   __syncwarp();
 }
 
-// Visited cache slot and tag of an id.  vc_bits = B > 0: ids are < 2^B and h = id * odd mod 2^B is a bijection of
-// [0, 2^B); the slot is h's top hbits and the tag its low B - hbits bits (+1, so 0 marks an empty slot), stored in 16
-// bits (B - hbits <= 15): equal tags in a slot mean equal ids, so the cache stays exact while holding twice the
-// entries of a u32 cache in the same shared memory.  B = 0: u32 entries holding the id itself (empty = 0xFFFFFFFF).
-__device__ __forceinline__ void cache_pos(uint32_t id, int hbits, int B, uint32_t& slot, uint32_t& tag) {
+// Visited cache slot and tag of an id, for a cache of M slots.  vc_bits = B > 0: ids are < 2^B and h = id * odd mod
+// 2^B is a bijection of [0, 2^B); slot = floor(h * M / 2^B), so the h of one slot form a contiguous run of at most
+// ceil(2^B / M) <= 2^tb values and their low tb bits (tmask = 2^tb - 1) tell them apart: tag = (h & tmask) + 1 (0
+// marks an empty slot), stored in 16 bits (tb <= 15).  Equal tags in a slot mean equal ids, so the cache stays exact
+// while holding twice the entries of a u32 cache in the same shared memory.  B = 0: u32 entries holding the id itself
+// (empty = 0xFFFFFFFF), slot = floor(h * M / 2^32) of the 32-bit hash.
+__device__ __forceinline__ void cache_pos(uint32_t id, uint32_t M, int B, uint32_t tmask, uint32_t& slot,
+                                          uint32_t& tag) {
   if (B) {
     const uint32_t h = (id * 0x9E3779B1u) & ((1u << B) - 1u);
-    slot = h >> (B - hbits);
-    tag = (h & ((1u << (B - hbits)) - 1u)) + 1u;
+    slot = (uint32_t)(((uint64_t)h * M) >> B);
+    tag = (h & tmask) + 1u;
   } else {
-    slot = (id * 0x9E3779B1u) >> (32 - hbits);
+    slot = (uint32_t)(((uint64_t)(id * 0x9E3779B1u) * M) >> 32);
     tag = id;
   }
 }
@@ -168,21 +166,23 @@ template <int CPL, int DQT>
 __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search_lp_kernel(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int MP = 32 * CPL;
+  // whole-warp rows (gather_keys_w) at D = 200 (Geo<50> teams of 16 lanes leave 14 of 64 float4 slots idle and hold
+  // 4 query float4 per lane); teams of Geo<DQT>::T lanes otherwise (D = 96 / 128: 8 lanes, no idle slots)
+  constexpr bool kLpWhole = SVF_LP_WHOLE && DQT == 50;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int VB = a.vc_bits;  // 16-bit tagged cache when > 0
-  const LpLayout lay{a.hbits, (a.L + 31) & ~31, MP, VB > 0, a.dq * 4};
+  const uint32_t M = (uint32_t)a.vc_slots, TM = a.vc_tmask;
+  const LpLayout lay{a.vc_slots, (a.L + 31) & ~31, MP, VB > 0, a.dq * 4};
   unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
-  float4* qs = reinterpret_cast<float4*>(base);
-  uint32_t* cache = reinterpret_cast<uint32_t*>(base + lay.cache_off());
-  uint16_t* cache16 = reinterpret_cast<uint16_t*>(base + lay.cache_off());
+  float4* qs = reinterpret_cast<float4*>(base);  // the query is staged in the cache region, then the cache cleared
+  uint32_t* cache = reinterpret_cast<uint32_t*>(base);
+  uint16_t* cache16 = reinterpret_cast<uint16_t*>(base);
   uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());
   uint32_t* sid = reinterpret_cast<uint32_t*>(base + lay.sid_off());
   uint64_t* skey = reinterpret_cast<uint64_t*>(base + lay.skey_off());
-  uint64_t* ck = reinterpret_cast<uint64_t*>(base + lay.ck_off());
-  uint32_t* cb = reinterpret_cast<uint32_t*>(base + lay.cb_off());
+  uint64_t* ck = skey;  // C.Update compacts the passing keys in place
   unsigned long long* qslot = reinterpret_cast<unsigned long long*>(base + lay.misc_off());
   uint32_t* spar = reinterpret_cast<uint32_t*>(base + lay.misc_off() + 16);
-  const int H = 1 << a.hbits;
   const int L = a.L;
 
   for (;;) {
@@ -208,34 +208,37 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     unsigned long long t_start = 0;
     if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    // S0: the query row into this warp's shared memory (coalesced, zero-padded to Dp), the visited cache cleared
+    // S0: the query row through this warp's cache region (coalesced, zero-padded to Dp) into registers, then the
+    // visited cache cleared
     const float* qg = a.Q + (size_t)qi * a.q_stride;
     float* qf32 = reinterpret_cast<float*>(qs);
     for (int i = lane; i < a.dq * 4; i += 32) qf32[i] = i < a.q_dim ? __ldcg(qg + i) : 0.f;
-#if !SVF_LP_QSMEM
     __syncwarp();
     float4 qv[4];
     {
-      const int T = DQT ? Geo<DQT>::T : a.team, tl = lane & (T - 1);
+      const int T = kLpWhole ? 32 : (DQT ? Geo<DQT>::T : a.team), tl = lane & (T - 1);
+      const int NV = kLpWhole ? (DQT + 31) / 32 : (DQT ? Geo<DQT>::NV : a.nv);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int c = tl + T * v;
-        qv[v] = (v < (DQT ? Geo<DQT>::NV : a.nv) && c < a.dq) ? qs[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qv[v] = (v < NV && c < a.dq) ? qs[c] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-#endif
+    __syncwarp();
     if (VB) {
-      for (int i = lane; i < (H >> 1); i += 32) cache[i] = 0u;
+      for (uint32_t i = lane; i < (M >> 1); i += 32) cache[i] = 0u;
     } else {
-      for (int i = lane; i < H; i += 32) cache[i] = kHashEmpty;
+      for (uint32_t i = lane; i < M; i += 32) cache[i] = kHashEmpty;
     }
     __syncwarp();
 
-#if SVF_LP_QSMEM
-#define GATHER_LP(S_) gather_keys_lp<DQT>(a, sid, skey, (S_), qs, lane)
-#else
-#define GATHER_LP(S_) gather_keys<DQT, (DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U)>(a, sid, skey, (S_), qv, lane)
-#endif
+#define GATHER_LP(S_, PF_)                                                                                     \
+  do {                                                                                                         \
+    if constexpr (kLpWhole)                                                                                    \
+      gather_keys_w<DQT, (DQT > 32 ? SVF_GATHER_W_LP / 2 : SVF_GATHER_W_LP)>(a, sid, skey, (S_), qv, lane, PF_); \
+    else                                                                                                       \
+      gather_keys<DQT, (DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U), true>(a, sid, skey, (S_), qv, lane, PF_);  \
+  } while (0)
     int np = 0;  // entries in the pool (<= L)
     int fu = 0;  // every entry before fu is parented
     uint32_t n_dist = 0, iters = 0, n_exp = 0;
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           uint32_t slot = 0, tag = 0;
           if (keep) {
             sid[pos] = id;
-            cache_pos(id, a.hbits, VB, slot, tag);
+            cache_pos(id, M, VB, TM, slot, tag);
           }
           // one writer per slot (the lowest lane), so the cache never sees two stores to one slot at once
           const unsigned peers = SVF_LP_ONE_WRITER
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         }
         const int kept = min(running, a.n_init - taken);
         taken += kept;
-        GATHER_LP(kept);
+        GATHER_LP(kept, 0ull);
         n_dist += kept;
         update(kept);
       }
@@ -411,20 +414,11 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));
         }
       }
+      // the best unparented entry after this iteration's parents is the next parent unless a new key beats it: pull
+      // its row toward L2 (no registers: the exact row is loaded after the merge, below)
       spec_id = kSent;
-      if (nxt < np) {
-        const uint32_t nid = key_id(pool[nxt]);
-        if (a.p == 1) {
-          spec_id = nid;
-#pragma unroll
-          for (int r = 0; r < CPL; ++r) {
-            const int e = r * 32 + lane;
-            spec_row[r] = e < a.R ? __ldg(a.graph + (size_t)spec_id * a.R + e) : kSent;
-          }
-        } else if (lane < ((a.R * 4 + 127) >> 7)) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.graph + (size_t)nid * a.R + lane * 32));
-        }
-      }
+      if (nxt < np && lane < ((a.R * 4 + 127) >> 7))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.graph + (size_t)key_id(pool[nxt]) * a.R + lane * 32));
       SVF_LPH(1)
       // S4: sentinel / snapshot / tombstone / visited-cache filters
       int running = 0;
@@ -435,7 +429,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         if (ok) ok = !tomb_dead(a.tomb, id);
         uint32_t slot = 0, tag = 0;
         if (ok) {
-          cache_pos(id, a.hbits, VB, slot, tag);
+          cache_pos(id, M, VB, TM, slot, tag);
           ok = VB ? cache16[slot] != (uint16_t)tag : cache[slot] != tag;
         }
         const unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -453,14 +447,15 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         running += __popc(m);
       }
       SVF_LPH(2)
-      if (running == 0) continue;
-      // S5 distances, S6 merge
-      GATHER_LP(running);
-      n_dist += running;
-      SVF_LPH(3)
-      update(running);
-      // p = 1: the next parent is now known exactly (pool[fu] is unparented whenever fu < np); if the speculative
-      // row is not its row, load the right one at once, so the fetch overlaps the next select
+      if (running > 0) {
+        // S5 distances (a new key better than the best unparented entry prefetches its row), S6 merge
+        GATHER_LP(running, fu < np ? (pool[fu] & ~1ull) : kEmptyKey);
+        n_dist += running;
+        SVF_LPH(3)
+        update(running);
+      }
+      // p = 1: the next parent is now known exactly (pool[fu] is unparented whenever fu < np); load its row at once
+      // (usually an L2 hit after the prefetches above), so the fetch overlaps the next select
       if (SVF_LP_EARLY_ROW && a.p == 1 && fu < np) {
         const uint32_t nid = key_id(pool[fu]);
         if (nid != spec_id) {
@@ -509,14 +504,14 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
 
 }  // namespace
 
-static inline size_t search_lp_smem_bytes(int hbits, int L, int cpl, int c16, int Dp) {
-  return kSearchWarpsPerBlock * LpLayout{hbits, (L + 31) & ~31, 32 * cpl, c16, Dp}.warp_bytes();
+static inline size_t search_lp_smem_bytes(int slots, int L, int cpl, int c16, int Dp) {
+  return kSearchWarpsPerBlock * LpLayout{slots, (L + 31) & ~31, 32 * cpl, c16, Dp}.warp_bytes();
 }
 
 template <int CPL, int DQT>
 static cudaError_t launch_lp_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   auto kern = search_lp_kernel<CPL, DQT>;
-  const size_t smem = search_lp_smem_bytes(a.hbits, a.L, CPL, a.vc_bits > 0, a.dq * 4);
+  const size_t smem = search_lp_smem_bytes(a.vc_slots, a.L, CPL, a.vc_bits > 0, a.dq * 4);
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0, cached_dev = -1;
   int dev = 0, per_sm = 0;

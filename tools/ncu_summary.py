@@ -9,6 +9,7 @@ import collections
 import csv
 import json
 import os
+import re
 import subprocess
 
 KEYS = [
@@ -84,7 +85,7 @@ def main():
         js["kernels"] = rep_summary(a.rep)
         # one search step = every captured search_kernel grid (the one-warp grid + the chained handoff grid)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        step = [k for k in js["kernels"] if "search_kernel" in k["kernel"]] or js["kernels"][:1]
+        step = [k for k in js["kernels"] if re.search(r"search(_lp)?_kernel", k["kernel"])] or js["kernels"][:1]
         if all(isinstance(k.get("dram__bytes_read.sum"), float) for k in step):
             tot = sum(k["dram__bytes_read.sum"] * scale.get(k["dram__bytes_read.sum.unit"], 1) +
                       k["dram__bytes_write.sum"] * scale.get(k["dram__bytes_write.sum.unit"], 1) for k in step)

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="base rows (0 = the config's)")
     ap.add_argument("--degree", type=int, default=64)
     ap.add_argument("--no-insert", action="store_true")
+    ap.add_argument("--hbits", default="0", help="visited-cache sizes 2^b to try (0 = the library's default)")
+    ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -45,9 +47,10 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     res = {"config": f"{a.config} graph at L_build {a.build_itopk}; queries = fresh insert vectors", "runs": []}
     idx.set_search_handoff(0)
-    for L in [int(x) for x in a.itopks.split(",")]:
-        for nq in [int(x) for x in a.batches.split(",")]:
-            idx.set_search_params(a.width, 0, 0, 0)
+    for L, nq, hb in [(L, nq, hb) for L in map(int, a.itopks.split(",")) for nq in map(int, a.batches.split(","))
+                      for hb in map(int, a.hbits.split(","))]:
+        if True:
+            idx.set_search_params(a.width, 0, 0, hb)
             Q = Qn[:nq].contiguous()
             for _ in range(2):
                 idx.search(Q, 10, L)
@@ -61,13 +64,20 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             c = idx.last_search_counters()
+            if a.no_trace:
+                row = {"itopk": L, "nq": nq, "width": a.width, "hbits": hb, "ms_median": round(float(np.median(ts)), 4),
+                       "n_dist_per_q": round(c["n_dist"] / c["queries"], 1),
+                       "iters_per_q": round(c["iters"] / c["queries"], 1)}
+                print(json.dumps(row), flush=True)
+                res["runs"].append(row)
+                continue
             idx.set_trace(True)
             flush.zero_()
             idx.search(Q, 10, L)
             torch.cuda.synchronize()
             r = analyse(*idx.read_trace(nq))
             idx.set_trace(False)
-            row = {"itopk": L, "nq": nq, "width": a.width, "ms_median": round(float(np.median(ts)), 4),
+            row = {"itopk": L, "nq": nq, "width": a.width, "hbits": hb, "ms_median": round(float(np.median(ts)), 4),
                    "n_dist_per_q": round(c["n_dist"] / c["queries"], 1), "iters_per_q": round(c["iters"] / c["queries"], 1),
                    **{k: r[k] for k in ("span_us", "drain_us", "after_drain_us", "dur_us", "ns_per_iter_median",
                                         "phase_cycles_per_iter")}}
