@@ -38,7 +38,7 @@ METRIC = "QPS at recall@10>=0.95 (batch 10K) and inserts/sec"
 # L_build per config (svf_params.build_itopk; reading I15): the graph is grown once at this candidate-list size, then
 # streamed inserts run at insert_itopk = 128.  Measured (profiles/r01_build_itopk.md): C2 at L_build 256 reaches
 # recall@10 0.974 at itopk 10; C4 at 10M: 0.70 -> 0.92 at itopk 128 with 512.
-BUILD_ITOPK = {"C1": 0, "C2": 256, "C3": 512, "C4": 512, "C5": 512}
+BUILD_ITOPK = {"C1": 0, "C2": 256, "C2G": 256, "C3": 512, "C4": 512, "C5": 512}
 # L_insert per config (svf_params.insert_itopk; default 128).  Kept > R: at L_insert <= R the detour selection
 # keeps every candidate (no pruning) and streamed rows drift toward a plain kNN graph.
 INSERT_ITOPK: dict = {}
@@ -46,7 +46,7 @@ INSERT_ITOPK: dict = {}
 # batch is used (I4: a cap ends a query's search early; 0 = run to convergence)
 MI_SWEEP = [64, 48, 40, 32, 28, 24, 20, 18, 16, 14, 12]
 SELECT_SEED = 3          # held-out query batch for choosing itopk and the cap (the timed batch is seed 2)
-EXTRA_CONFIGS = ["C3", "C4"]
+EXTRA_CONFIGS = ["C3", "C4", "C2G"]
 
 
 def mi_caps(L: int) -> list:

@@ -215,7 +215,9 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   // 7.1 vs 7.2 ms; tools/param_sweep.py, tools/insert_rate.py)
   // 4096 slots for 128 < L <= 256 (C4 2M x 200, L_build 512: itopk 192 27.5 -> 15.4 ms, 256 37.6 -> 19.7 ms vs
   // 8192 slots, identical results; 2048 slots is 2% faster again but recomputes 1.6x; profiles/c4_2m_hash.json)
-  const int autobits = L <= 16 ? 10 : (L <= 128 ? 11 : (L <= 256 ? 12 : 13));
+  // 1024 slots up to L = 32 (C3 itopk 20 cap 35, round 2: 1.050 -> 1.001 ms per 10K batch, 6 blocks/SM instead of 5;
+  // 512 slots: 1.044 ms; C2 itopk 10: 512 slots 0.599 vs 0.573 ms; profiles/r02_ks_ab.json)
+  const int autobits = L <= 32 ? 10 : (L <= 128 ? 11 : (L <= 256 ? 12 : 13));
   // K-S-L for pools of more than 64 keys (one warp per query): its direct-mapped visited cache needs no load
   // invariant, only room to stage the query row
   c.lp = LP > 64 && idx->wpq != 2 && lp_enabled();

@@ -529,12 +529,14 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
       // registers when the guess was right
       uint32_t rowv[CPL];
       const bool hit = np == 1 && spar[0] == spec_id;
+      if (TMA_ROW && hit) row_settle();  // the bulk copy of the guessed row has landed in rowbuf
       for (int r = 0; r < CPL; ++r) {
         const int e = r * 32 + lane;
         rowv[r] = kSent;
         if ((r % WPQ) != h) continue;
         if (hit) {
-          rowv[r] = spec_row[r];
+          if (TMA_ROW) rowv[r] = e < a.R ? rowbuf[e] : kSent;
+          else rowv[r] = spec_row[r];
         } else if (e < ncand) {
           const int pi = a.rshift >= 0 ? (e >> a.rshift) : e / a.R;
           rowv[r] = __ldg(a.graph + (size_t)spar[pi] * a.R + (e - pi * a.R));

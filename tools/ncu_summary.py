@@ -78,6 +78,7 @@ def main():
     ap.add_argument("--itopk", type=int, default=0)
     ap.add_argument("--out", required=True)
     ap.add_argument("--latest", action="store_true")
+    ap.add_argument("--config", default="C2", help="with --latest: which config's traffic file bench.py reads")
     ap.add_argument("--note", default="")
     a = ap.parse_args()
     js = {"note": a.note, "nq": a.nq, "itopk": a.itopk}
@@ -112,7 +113,8 @@ def main():
     if a.latest and "dram_bytes_per_query" in js:
         json.dump({"itopk": a.itopk, "dram_bytes_per_query": js["dram_bytes_per_query"],
                    "source": os.path.basename(a.out) + ".json"},
-                  open(os.path.join(os.path.dirname(a.out), "ncu_search_latest.json"), "w"), indent=1)
+                  open(os.path.join(os.path.dirname(a.out), "ncu_search_latest.json" if a.config == "C2"
+                                    else f"ncu_search_latest_{a.config}.json"), "w"), indent=1)
     print(json.dumps({k: v for k, v in js.items() if k != "kernels"}, indent=1)[:2000])
 
 

@@ -140,6 +140,11 @@ CONFIGS = {
     "C2": dict(workload="C2: SIFT1M-shaped 1M x d128 fp32 (integer-valued G-LM), R=64, 10K-query batch, k=10, L2",
                n=1_000_000, dim=128, degree=64, nq=10_000, k=10, metric=0,
                gen=GLM(dim=128, ell=32, s=30.0, m=64.0, sigma=2.0, integer=True), ood=False),
+    # SURVEY §8(d) C2 "second curve on G-CL (1024 clusters)": the stress generator at C2's shape
+    "C2G": dict(workload="C2G: C2 shape (1M x d128 integer-valued, R=64, 10K queries, L2) on the G-CL stress generator "
+                         "(1024 clusters, rank-12 subspaces)",
+                n=1_000_000, dim=128, degree=64, nq=10_000, k=10, metric=0,
+                gen=GCL(dim=128, n_clusters=1024), ood=False),
     "C3": dict(workload="C3: Deep10M-shaped 10M x d96 unit-norm G-LM, R=64, 10K queries, streaming 1% ins/del",
                n=10_000_000, dim=96, degree=64, nq=10_000, k=10, metric=0,
                gen=GLM(dim=96, ell=24, s=1.0, m=0.0, sigma=0.05, normalize=True), ood=False),
