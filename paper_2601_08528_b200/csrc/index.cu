@@ -192,8 +192,10 @@ int lp_cache_slots(const svf_index* idx, int L, int cpl, bool c16) {
   // 1 KB per block is reserved by the system; blocks are allocated in 128-byte units
   const long per_block = ((long)idx->smem_sm / SVF_MINB_LP - 1024) & ~127L;
   const long per_warp = (per_block / kSearchWarpsPerBlock) & ~15L;
-  // all but the cache: the per-warp layout with an 8-slot cache, minus those 8 slots
-  const long fixed = (long)search_smem_bytes(8, 0, cpl, L, 1, c16 ? 1 : 0, 0, 8) / kSearchWarpsPerBlock - 8 * (c16 ? 2 : 4);
+  // all but the cache: the per-warp layout with an 8-slot cache, minus that cache region (which also stages the
+  // query row, so it is at least Dp floats)
+  const long c8 = ((std::max<long>(8L * (c16 ? 2 : 4), (long)idx->Dp * 4)) + 15) & ~15L;
+  const long fixed = (long)search_smem_bytes(8, 0, cpl, L, 1, c16 ? 1 : 0, idx->Dp, 8) / kSearchWarpsPerBlock - c8;
   const long m = (per_warp - fixed) / (c16 ? 2 : 4);
   return (int)std::max(256L, m & ~7L);
 }

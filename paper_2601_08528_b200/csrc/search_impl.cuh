@@ -115,9 +115,20 @@ __device__ __forceinline__ void prefetch_graph_row(const uint32_t* graph, int R,
   for (int b = 0; b < R * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
 }
 
-template <int DQT, int U, bool PF = false>
+// Where a gather reads the query: this lane's NV float4 held in registers (K-S), or the row in shared memory (K-S-L
+// with SVF_LP_QSMEM: 16 registers at D = 128 go to rows in flight instead)
+struct QueryRegs {
+  const float4 (&q)[4];
+  __device__ __forceinline__ float4 operator()(int v, int) const { return q[v]; }
+};
+struct QuerySmem {
+  const float4* q;
+  __device__ __forceinline__ float4 operator()(int, int c) const { return q[c]; }
+};
+
+template <int DQT, int U, bool PF = false, class QF = QueryRegs>
 __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t* sid, uint64_t* skey, int S,
-                                            const float4 (&qv)[4], int lane, uint64_t pf = 0ull) {
+                                            const QF& qf, int lane, uint64_t pf = 0ull) {
   const int T = DQT ? Geo<DQT>::T : a.team, NV = DQT ? Geo<DQT>::NV : a.nv, DQ = DQT ? DQT : a.dq;
   const int tl = lane & (T - 1), team = lane / T, nteams = 32 / T;
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
@@ -153,7 +164,12 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
       constexpr int NVC = DQT ? Geo<DQT>::NV : 4;  // float4 per lane per row (the generic path pads with zeros)
       uint64_t acc2 = 0ull;
 #pragma unroll
-      for (int v = 0; v < NVC; ++v) acc2 = dist_acc4(acc2, xv[u][v], qv[v], a.metric);
+      for (int v = 0; v < NVC; ++v) {
+        const int c = tl + T * v;  // lanes past the row (generic / inexact geometries) hold zeros on both sides
+        const float4 q = (DQT > 0 && Geo<DQT>::T * Geo<DQT>::NV == DQT) || (v < NV && c < DQ) ? qf(v, c)
+                                                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc2 = dist_acc4(acc2, xv[u][v], q, a.metric);
+      }
       float acc = f2sum(acc2);
       if (DQT) {
 #pragma unroll
@@ -178,7 +194,7 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
 template <int KPL, int CPL, int DQT, int U>
 __device__ __forceinline__ int score_own(const SearchArgs& a, const uint64_t (&pool)[KPL], const uint32_t* sid,
                                          uint64_t* skey, int S, const float4 (&qv)[4], int lane) {
-  gather_keys<DQT, U>(a, sid, skey, S, qv, lane);
+  gather_keys<DQT, U>(a, sid, skey, S, QueryRegs{qv}, lane);
   uint64_t kreg = kEmptyKey;
 #pragma unroll
   for (int r = 0; r < KPL; ++r)

@@ -24,6 +24,12 @@ namespace svf {
 
 namespace {
 
+// SVF_LP_QSMEM = 1: the team gather (D = 96 / 128) reads the query from a shared-memory copy instead of 4 float4
+// registers per lane, which removes the spills at the 72-register cap (C2 itopk 128: 4096 queries 1.438 -> 1.412 ms,
+// 10K 3.057 -> 3.017 ms; itopk 96 10K 2.474 -> 2.428 ms; profiles/r02_lp_ab.json)
+#ifndef SVF_LP_QSMEM
+#define SVF_LP_QSMEM 1
+#endif
 // per-warp shared memory: [visited cache M entries (u16 tags or u32 ids); the query row is staged here before the
 // cache is cleared | pool Lp u64 | survivor ids MP u32 | keys MP u64 (compacted in place by C.Update) | query slot
 // 2 u64 | parents 8 u32].  M need not be a power of two (slot = multiply-shift of a hashed id), so the launcher
@@ -34,7 +40,8 @@ struct LpLayout {
     const size_t cb = (size_t)M * (c16 ? 2 : 4), qb = (size_t)Dp * 4;
     return ((cb > qb ? cb : qb) + 15) & ~(size_t)15;
   }
-  __host__ __device__ size_t pool_off() const { return cache_bytes(); }
+  __host__ __device__ size_t qs_off() const { return cache_bytes(); }  // SVF_LP_QSMEM: a resident query copy
+  __host__ __device__ size_t pool_off() const { return qs_off() + (SVF_LP_QSMEM ? (((size_t)Dp * 4 + 15) & ~(size_t)15) : 0); }
   __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
   __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
   __host__ __device__ size_t misc_off() const { return skey_off() + (size_t)MP * 8; }
@@ -174,7 +181,8 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   const uint32_t M = (uint32_t)a.vc_slots, TM = a.vc_tmask;
   const LpLayout lay{a.vc_slots, (a.L + 31) & ~31, MP, VB > 0, a.dq * 4};
   unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
-  float4* qs = reinterpret_cast<float4*>(base);  // the query is staged in the cache region, then the cache cleared
+  // the query is staged in the cache region (then the cache is cleared), or kept in its own region (SVF_LP_QSMEM)
+  float4* qs = reinterpret_cast<float4*>(base + (SVF_LP_QSMEM ? lay.qs_off() : 0));
   uint32_t* cache = reinterpret_cast<uint32_t*>(base);
   uint16_t* cache16 = reinterpret_cast<uint16_t*>(base);
   uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());
@@ -232,12 +240,17 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
     }
     __syncwarp();
 
+#if SVF_LP_QSMEM
+#define QSRC QuerySmem{qs}
+#else
+#define QSRC QueryRegs{qv}
+#endif
 #define GATHER_LP(S_, PF_)                                                                                     \
   do {                                                                                                         \
     if constexpr (kLpWhole)                                                                                    \
       gather_keys_w<DQT, (DQT > 32 ? SVF_GATHER_W_LP / 2 : SVF_GATHER_W_LP)>(a, sid, skey, (S_), qv, lane, PF_); \
     else                                                                                                       \
-      gather_keys<DQT, (DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U), true>(a, sid, skey, (S_), qv, lane, PF_);  \
+      gather_keys<DQT, (DQT > 0 ? SVF_GATHER_U_LP : SVF_GATHER_U), true>(a, sid, skey, (S_), QSRC, lane, PF_);  \
   } while (0)
     int np = 0;  // entries in the pool (<= L)
     int fu = 0;  // every entry before fu is parented
