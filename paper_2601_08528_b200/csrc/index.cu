@@ -154,6 +154,7 @@ int pow2_at_least(int x) {
 struct SearchCfg {
   int kpl, cpl, hbits, team, nv, n_init, wpq, lp, vc_bits, vc_slots;
   uint32_t vc_tmask;
+  bool lp_auto;  // K-S-L cache sized by the launcher (no hash_bits / SVF_LP_BITS)
 };
 
 // K-S-L (shared-memory pool kernel) for pools of more than 64 keys; SVF_LP=0 keeps the register-pool kernel (A/B)
@@ -187,10 +188,10 @@ int lp_bits_env() {
 // cache gets whatever shared memory that residency leaves once the pool and buffers are placed (C2 L_insert 128: 3120
 // 16-bit slots, C4 itopk 192: 2864; a power-of-two 2048 before round 2 recomputed 1.5x the oracle's distances, and
 // 4096 cost two blocks/SM: profiles/r02_lp_cache.json); larger pools keep 4096 slots at lower residency.
-int lp_cache_slots(const svf_index* idx, int L, int cpl, bool c16) {
+int lp_cache_slots(const svf_index* idx, int L, int cpl, bool c16, int minb) {
   if (L > 256) return 4096;
   // 1 KB per block is reserved by the system; blocks are allocated in 128-byte units
-  const long per_block = ((long)idx->smem_sm / SVF_MINB_LP - 1024) & ~127L;
+  const long per_block = ((long)idx->smem_sm / minb - 1024) & ~127L;
   const long per_warp = (per_block / kSearchWarpsPerBlock) & ~15L;
   // all but the cache: the per-warp layout with an 8-slot cache, minus that cache region (which also stages the
   // query row, so it is at least Dp floats)
@@ -198,6 +199,30 @@ int lp_cache_slots(const svf_index* idx, int L, int cpl, bool c16) {
   const long fixed = (long)search_smem_bytes(8, 0, cpl, L, 1, c16 ? 1 : 0, idx->Dp, 8) / kSearchWarpsPerBlock - c8;
   const long m = (per_warp - fixed) / (c16 ? 2 : 4);
   return (int)std::max(256L, m & ~7L);
+}
+
+// K-S-L visited cache of a configuration: 2^bits slots, or (bits = 0) sized for `minb` resident blocks per SM
+void lp_cache_cfg(const svf_index* idx, int L, int cpl, int bits, int minb, SearchCfg& c) {
+  // ids are < 2^B; 16-bit tags when a slot's run of hashed ids, ceil(2^B / M), fits 15 bits (DESIGN §6 K-S-L)
+  int B = 1;
+  while (B < 32 && ((int64_t)1 << B) < idx->cap) ++B;
+  auto fits16 = [&](int M) {
+    const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
+    return B <= 31 && run <= 32768 && !lp_u32_cache();
+  };
+  int M = bits > 0 ? (1 << std::min(bits, 16)) : lp_cache_slots(idx, L, cpl, true, minb);
+  c.vc_bits = fits16(M) ? B : 0;
+  if (!c.vc_bits && bits == 0) M = lp_cache_slots(idx, L, cpl, false, minb);
+  c.vc_slots = M;
+  c.vc_tmask = 0;
+  if (c.vc_bits) {
+    const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
+    int tb = 0;
+    while (((uint64_t)1 << tb) < run) ++tb;
+    c.vc_tmask = (1u << tb) - 1u;
+  }
+  c.hbits = 8;
+  while ((1 << c.hbits) < M) ++c.hbits;  // reported only (svf_last_search_counters); K-S-L uses vc_slots
 }
 
 bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, SearchCfg& c, std::string& why) {
@@ -226,27 +251,11 @@ bool search_cfg(const svf_index* idx, int L, int p, int n_init, int hash_bits, S
   c.vc_bits = 0;
   c.vc_slots = 0;
   c.vc_tmask = 0;
+  c.lp_auto = false;
   if (c.lp) {
-    // ids are < 2^B; 16-bit tags when a slot's run of hashed ids, ceil(2^B / M), fits 15 bits (DESIGN §6 K-S-L)
-    int B = 1;
-    while (B < 32 && ((int64_t)1 << B) < idx->cap) ++B;
     const int bits = hash_bits > 0 ? std::max(hash_bits, 8) : lp_bits_env();
-    auto fits16 = [&](int M) {
-      const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
-      return B <= 31 && run <= 32768 && !lp_u32_cache();
-    };
-    int M = bits > 0 ? (1 << std::min(bits, 16)) : lp_cache_slots(idx, L, c.cpl, true);
-    c.vc_bits = fits16(M) ? B : 0;
-    if (!c.vc_bits && bits == 0) M = lp_cache_slots(idx, L, c.cpl, false);
-    c.vc_slots = M;
-    if (c.vc_bits) {
-      const uint64_t run = (((uint64_t)1 << B) + M - 1) / M;
-      int tb = 0;
-      while (((uint64_t)1 << tb) < run) ++tb;
-      c.vc_tmask = (1u << tb) - 1u;
-    }
-    c.hbits = 8;
-    while ((1 << c.hbits) < M) ++c.hbits;  // reported only (svf_last_search_counters); K-S-L uses vc_slots
+    c.lp_auto = bits == 0;
+    lp_cache_cfg(idx, L, c.cpl, bits, SVF_MINB_LP, c);
   } else {
     c.hbits = hash_bits > 0 ? std::max(hash_bits, minbits) : std::max(autobits, minbits);
   }
@@ -398,9 +407,16 @@ cudaError_t run_search(svf_index* idx, const float* Q, int64_t q_stride, int q_d
   a.wpq = c.wpq;
   if (idx->wpq == 0) a.wpq = (c.cpl >= 2 && c.kpl <= 4 && 2 * nq <= 24LL * idx->num_sms) ? 2 : 1;
   a.large_pool = c.lp && a.wpq == 1;
-  a.vc_bits = c.vc_bits;
-  a.vc_slots = c.vc_slots;
-  a.vc_tmask = c.vc_tmask;
+  SearchCfg cl = c;
+  // wide rows (D >= 192: DRAM-bound, ncu C4 67% of DRAM peak) in a batch of more than ~1.25 waves of the 7-block
+  // residency: the K-S-L cache is sized for 6 blocks/SM, trading residency for fewer recomputed 800-byte rows (C4
+  // itopk 192 10K: 10.74-10.94 -> 10.52 ms, 6018 -> 5878 distances per query).  At D = 128 (38% of DRAM peak) the
+  // same trade was slower (C2 itopk 128 10K 3.017 -> 3.049 ms), and a 4,096-query insert sub-batch keeps one wave.
+  if (a.large_pool && c.lp_auto && idx->Dp >= 192 && nq * 4 > 5LL * SVF_MINB_LP * kSearchWarpsPerBlock * idx->num_sms)
+    lp_cache_cfg(idx, L, c.cpl, 0, SVF_MINB_LP - 1, cl);
+  a.vc_bits = cl.vc_bits;
+  a.vc_slots = cl.vc_slots;
+  a.vc_tmask = cl.vc_tmask;
   cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   unsigned long long*& hob = update_path ? idx->ho_upd : idx->ho;

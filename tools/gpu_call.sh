@@ -1,8 +1,7 @@
-# insert: detour selection PDL-chained behind the insert search (per-vertex done flags) vs serial
-O=gpurun_out/q
+# full GPU tests + smoke + the default bench (C2 headline, C3, C4, C2G) + the reference (oracle) arm
+O=gpurun_out/t
 mkdir -p $O
-timeout 300 python -m pytest tests/test_gpu_parity.py -q -x --timeout 120 -k "insert or build or large_pool" > $O/parity1.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_traces.py -q -x --timeout 120 > $O/parity.log 2>&1
-for ch in 1 0; do
-  SVF_INS_CHAIN=$ch timeout 300 python tools/pool_probe.py --itopks 128 --batches 4096 --no-trace --out $O/c2_chain$ch.json > $O/c2_chain$ch.log 2>&1
-done
+(time timeout 2400 python -m pytest tests -m gpu -q -rf --timeout 900) > $O/gpu_tests.log 2>&1
+(time timeout 300 python -c "import __graft_entry__ as g; g.smoke()") > $O/smoke.log 2>&1
+(time timeout 2400 python bench.py) > $O/bench.json 2> $O/bench.err
+(time timeout 1200 python bench.py --impl reference --steps 3 --warmup 1) > $O/bench_ref.json 2> $O/bench_ref.err

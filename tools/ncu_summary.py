@@ -86,7 +86,12 @@ def main():
         js["kernels"] = rep_summary(a.rep)
         # one search step = every captured search_kernel grid (the one-warp grid + the chained handoff grid)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        step = [k for k in js["kernels"] if re.search(r"search(_lp)?_kernel", k["kernel"])] or js["kernels"][:1]
+        step, seen = [], set()
+        for k in js["kernels"]:  # one step = each distinct search grid once (a capture may hold two steps)
+            if re.search(r"search(_lp)?_kernel", k["kernel"]) and k["kernel"] not in seen:
+                seen.add(k["kernel"])
+                step.append(k)
+        step = step or js["kernels"][:1]
         if all(isinstance(k.get("dram__bytes_read.sum"), float) for k in step):
             tot = sum(k["dram__bytes_read.sum"] * scale.get(k["dram__bytes_read.sum.unit"], 1) +
                       k["dram__bytes_write.sum"] * scale.get(k["dram__bytes_write.sum.unit"], 1) for k in step)
