@@ -145,6 +145,10 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
 #elif SVF_PREFETCH == 1
   prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
 #endif
+  // the team geometry covers a row exactly at D = 96 / 128 (T * NV = DQ): rows load unconditionally (a slot past S
+  // re-reads survivor 0's row, an L1 hit, and its key is never stored); other widths keep the per-lane guards
+  constexpr bool kExact = PF && DQT > 0 && Geo<DQT>::T * Geo<DQT>::NV == DQT;  // K-S-L only (K-S keeps its guards)
+  constexpr int NVC = DQT ? Geo<DQT>::NV : 4;  // float4 per lane per row (the generic path pads with zeros)
   for (int base = 0; base < S; base += nteams * U) {
     float4 xv[U][4];
     uint32_t id[U];
@@ -152,25 +156,30 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
     for (int u = 0; u < U; ++u) {
       const int s = base + team + nteams * u;
       id[u] = s < S ? sid[s] : kSent;
-      const float4* row = vec4 + (size_t)(id[u] == kSent ? 0 : id[u]) * DQ;
+      const float4* row = vec4 + (size_t)(kExact ? sid[s < S ? s : 0] : (id[u] == kSent ? 0 : id[u])) * DQ;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
+      for (int v = 0; v < NVC; ++v) {
         const int c = tl + T * v;
-        xv[u][v] = (v < NV && c < DQ && id[u] != kSent) ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kExact)
+          xv[u][v] = __ldg(row + c);
+        else
+          xv[u][v] = (v < NV && c < DQ && id[u] != kSent) ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    }
+    // one query float4 per v serves every row of the round (read once from shared memory in K-S-L)
+    uint64_t acc2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc2[u] = 0ull;
+#pragma unroll
+    for (int v = 0; v < NVC; ++v) {
+      const int c = tl + T * v;  // lanes past the row (generic / inexact geometries) hold zeros on both sides
+      const float4 q = kExact || (v < NV && c < DQ) ? qf(v, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc2[u] = dist_acc4(acc2[u], xv[u][v], q, a.metric);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      constexpr int NVC = DQT ? Geo<DQT>::NV : 4;  // float4 per lane per row (the generic path pads with zeros)
-      uint64_t acc2 = 0ull;
-#pragma unroll
-      for (int v = 0; v < NVC; ++v) {
-        const int c = tl + T * v;  // lanes past the row (generic / inexact geometries) hold zeros on both sides
-        const float4 q = (DQT > 0 && Geo<DQT>::T * Geo<DQT>::NV == DQT) || (v < NV && c < DQ) ? qf(v, c)
-                                                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-        acc2 = dist_acc4(acc2, xv[u][v], q, a.metric);
-      }
-      float acc = f2sum(acc2);
+      float acc = f2sum(acc2[u]);
       if (DQT) {
 #pragma unroll
         for (int off = Geo<DQT>::T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
