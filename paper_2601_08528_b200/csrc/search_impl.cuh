@@ -177,18 +177,23 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
 #pragma unroll
       for (int u = 0; u < U; ++u) acc2[u] = dist_acc4(acc2[u], xv[u][v], q, a.metric);
     }
+    // every row's team reduction first (converged shuffles), then the divergent key stores
+    float acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      float acc = f2sum(acc2[u]);
+      acc[u] = f2sum(acc2[u]);
       if (DQT) {
 #pragma unroll
-        for (int off = Geo<DQT>::T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        for (int off = Geo<DQT>::T >> 1; off > 0; off >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
       } else {
-        for (int off = T >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        for (int off = T >> 1; off > 0; off >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
       }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
       const int s = base + team + nteams * u;
       if (tl == 0 && s < S) {
-        float d = (a.metric == 0 ? acc : -acc) + 0.0f;  // canonical +0
+        float d = (a.metric == 0 ? acc[u] : -acc[u]) + 0.0f;  // canonical +0
         const uint64_t key = make_key(d, id[u]);
         skey[s] = key;
         if (PF && key < pf) prefetch_graph_row(a.graph, a.R, id[u]);

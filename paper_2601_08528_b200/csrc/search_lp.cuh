@@ -284,10 +284,8 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           b = lower_bound_key(pool, np, c);
           keep = !(b < np && (pool[b] & ~1ull) == c);  // already in the pool (the cache forgot it)
         }
-        for (int i = 0; i < nh; ++i) {                 // the same id offered twice (p > 1): keep the first copy
-          const uint64_t ci = __shfl_sync(0xffffffffu, c, i);
-          if (i < lane && ci == c) keep = false;
-        }
+        // the same id offered twice (p > 1): keep the first copy (lanes >= nh hold kEmptyKey and keep = false)
+        if ((__match_any_sync(0xffffffffu, c) & ((1u << lane) - 1u)) != 0u) keep = false;
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (km == 0u) continue;
         int rank = 0;
@@ -298,13 +296,22 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         int b0 = keep ? b : L;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) b0 = min(b0, __shfl_xor_sync(0xffffffffu, b0, off));
+        int* hist = reinterpret_cast<int*>(sid);  // 32 counters (sid is free between the gather and the filter)
         for (int s0 = b0 + ((np - b0 - 1) & ~31); np > b0 && s0 >= b0; s0 -= 32) {  // back to front
           const int i = s0 + lane;
-          int cnt = 0;
-          for (int j = 0; j < nh; ++j) {
-            const int bj = __shfl_sync(0xffffffffu, b, j);
-            cnt += ((km >> j) & 1u) && bj <= i;
+          // cnt(i) = kept keys with b <= i: those below the chunk, plus an inclusive scan of the chunk's histogram
+          int cnt = __popc(__ballot_sync(0xffffffffu, keep && b < s0));
+          hist[lane] = 0;
+          __syncwarp();
+          if (keep && b >= s0 && b < s0 + 32) atomicAdd(hist + (b - s0), 1);
+          __syncwarp();
+          int h = hist[lane];
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, h, off);
+            if (lane >= off) h += t;
           }
+          cnt += h;
           const uint64_t pk = i < np ? pool[i] : 0ull;
           __syncwarp();
           if (i < np && i + cnt < L) pool[i + cnt] = pk;

@@ -1,5 +1,5 @@
 # K-S-L gather: unconditional row loads at exact geometries, one query float4 per v per round
-O=gpurun_out/u
+O=gpurun_out/v
 mkdir -p $O
 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x --timeout 120 > $O/parity.log 2>&1
 timeout 600 python tools/pool_probe.py --itopks 128 --batches 4096,10000 --no-trace --out $O/c2.json > $O/c2.log 2>&1
