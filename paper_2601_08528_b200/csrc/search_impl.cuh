@@ -112,7 +112,9 @@ __device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4
 // computed it pulls that id's neighbour row toward L2 at once; the exact row load after the merge then hits L2.
 __device__ __forceinline__ void prefetch_graph_row(const uint32_t* graph, int R, uint32_t id) {
   const char* p = reinterpret_cast<const char*>(graph + (size_t)id * R);
-  for (int b = 0; b < R * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  if (R > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128));  // R = 64: two lines
+  for (int b = 256; b < R * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
 }
 
 // Where a gather reads the query: this lane's NV float4 held in registers (K-S), or the row in shared memory (K-S-L
@@ -155,8 +157,15 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int s = base + team + nteams * u;
-      id[u] = s < S ? sid[s] : kSent;
-      const float4* row = vec4 + (size_t)(kExact ? sid[s < S ? s : 0] : (id[u] == kSent ? 0 : id[u])) * DQ;
+      uint32_t rid;
+      if (kExact) {  // one shared-memory read: slots past S re-read survivor 0
+        rid = sid[s < S ? s : 0];
+        id[u] = s < S ? rid : kSent;
+      } else {
+        id[u] = s < S ? sid[s] : kSent;
+        rid = id[u] == kSent ? 0 : id[u];
+      }
+      const float4* row = vec4 + (size_t)rid * DQ;
 #pragma unroll
       for (int v = 0; v < NVC; ++v) {
         const int c = tl + T * v;

@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (km == 0u) continue;
         int rank = 0;
-        for (int i = 0; i < nh; ++i) {
-          const uint64_t ci = __shfl_sync(0xffffffffu, c, i);
-          rank += ((km >> i) & 1u) && ci < c;
+        for (unsigned mk = km; mk != 0u; mk &= mk - 1u) {  // over the kept keys only
+          const uint64_t ci = __shfl_sync(0xffffffffu, c, __ffs(mk) - 1);
+          rank += ci < c;
         }
         int b0 = keep ? b : L;
 #pragma unroll
