@@ -147,6 +147,24 @@ def test_large_pool_kernel_bit_exact(svf, dim, L, p, bits, metric):
     assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
 
 
+def test_large_pool_cache_sizing_paths_bit_exact(svf):
+    """The launcher sizes K-S-L's visited cache at run time (DESIGN §6 K-S-L): any slot count M (multiply-shift slots,
+    16-bit tags over contiguous hash runs) for the 7-block residency, and -- for a multi-wave batch of wide rows
+    (D >= 192, more than ~1.25 waves) -- the larger cache of the 6-block residency.  Both paths must give O2 exactly:
+    D = 200 inner product, 5,400 queries (above the multi-wave threshold of a 148-SM B200) and 300 (below it)."""
+    gen = GLM(dim=200, ell=8, integer=True)
+    X = gen.rows(11, 11, 0, 5000) - 100.0
+    g, _ = oracle.build(X, R=32, seed_size=1000, B_ins=1000, L_ins=64, metric=1)
+    Q = gen.rows(11, 12, 0, 5400) - 100.0
+    idx = svf.Index.from_state(X, g, metric=1)
+    for nq in (5400, 300):
+        ids, d = idx.search(cuda(Q[:nq]), 10, 128)
+        ri, rd, rc = oracle.graph_search(X, g, Q[:nq], 10, 128, metric=1)
+        assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
+        cnt = idx.last_search_counters()
+        assert cnt["iters"] == rc[:, 2].sum() and cnt["n_dist"] >= rc[:, 0].sum()
+
+
 def test_two_new_vertices_in_one_sub_batch(svf):
     """The hand-derived sub-batch pin of tests/test_oracle_pins.py through svf_insert: inserted together, vertex 5
     does not reach vertex 4 although 4 is its nearest (snapshot semantics, I13); the rows and reverse edges equal the
