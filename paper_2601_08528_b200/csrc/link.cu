@@ -245,6 +245,9 @@ __global__ void segment_heads_kernel(const uint32_t* __restrict__ ku, int64_t n,
 // One warp per target u: tail(u) <- first (R-P) of sort_eff(tail(u) U requests(u)); prefix untouched; rows of
 // deleted u are frozen.  Tombstoned / empty tail entries count as +inf but keep their stored distance.
 // ET = registers per lane for the tail (R-P <= 32*ET); requests arrive in 32-wide chunks (typically 1-3 per target).
+// a target with at most this many reverse requests inserts them one by one instead of sorting and merging them
+constexpr int kFewRequests = 6;
+
 template <int ET>
 __global__ void __launch_bounds__(kLinkWarps * 32)
     reverse_apply_kernel(uint32_t* __restrict__ graph, float* __restrict__ edge_dist,
@@ -295,11 +298,31 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
     }
     if (!__all_sync(0xffffffffu, sorted)) warp_sort<ET>(best, lane);
     __syncwarp();
-    for (int64_t c0 = start; c0 < end; c0 += 32) {
-      uint64_t cand[1];
-      cand[0] = c0 + lane < end ? kv[c0 + lane] : kEmptyKey;
-      warp_sort<1>(cand, lane);
-      warp_merge_into<ET, 1>(best, cand, lane);
+    if (end - start <= kFewRequests) {
+      // few requests (the common case): insert each by its rank in the sorted tail (one ballot per register) and
+      // a one-slot shift, dropping the last -- the same first TS of tail U requests as the sort + merge below
+      for (int64_t i = start; i < end; ++i) {
+        const uint64_t c = kv[i];
+        int pos = 0;
+#pragma unroll
+        for (int r = 0; r < ET; ++r) pos += __popc(__ballot_sync(0xffffffffu, best[r] < c));
+        if (pos >= TS) continue;
+#pragma unroll
+        for (int r = ET - 1; r >= 0; --r) {
+          const uint64_t carry = __shfl_sync(0xffffffffu, best[r > 0 ? r - 1 : 0], 31);
+          uint64_t up = __shfl_up_sync(0xffffffffu, best[r], 1);
+          if (lane == 0) up = carry;
+          const int g = r * 32 + lane;
+          best[r] = g >= TS ? kEmptyKey : (g > pos ? up : (g == pos ? c : best[r]));  // the last drops out
+        }
+      }
+    } else {
+      for (int64_t c0 = start; c0 < end; c0 += 32) {
+        uint64_t cand[1];
+        cand[0] = c0 + lane < end ? kv[c0 + lane] : kEmptyKey;
+        warp_sort<1>(cand, lane);
+        warp_merge_into<ET, 1>(best, cand, lane);
+      }
     }
 #pragma unroll
     for (int r = 0; r < ET; ++r) {
