@@ -1,4 +1,3 @@
-O=gpurun_out/aa
+O=gpurun_out/ac
 mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_traces.py -q -x --timeout 300 > $O/parity.log 2>&1
-timeout 600 python tools/pool_probe.py --itopks 128 --batches 4096 --no-trace --out $O/c2.json > $O/c2.log 2>&1
+timeout 600 python tools/pool_probe.py --itopks 128 --batches 1808,2500,3334,4096,5000 --no-trace --no-insert --out $O/c2.json > $O/c2.log 2>&1
