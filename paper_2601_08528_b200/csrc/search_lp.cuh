@@ -536,17 +536,24 @@ static cudaError_t launch_lp_cpl(SearchArgs a, int num_sms, cudaStream_t st) {
   const size_t smem = search_lp_smem_bytes(a.vc_slots, a.L, CPL, a.vc_bits > 0, a.dq * 4);
   static thread_local size_t cached_smem = 0;
   static thread_local int cached_per_sm = 0, cached_dev = -1;
+  // the opt-in limit is only ever raised: a CUDA graph captured with the larger (6-block) cache must stay launchable
+  // after a 7-block launch (an insert) on the same function
+  static thread_local size_t attr_smem[16] = {};
   int dev = 0, per_sm = 0;
   cudaGetDevice(&dev);
   if (cached_smem == smem && cached_dev == dev) {
     per_sm = cached_per_sm;
   } else {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    // keep the L1 side large (in-flight gather lines), ask for just enough shared memory for the target residency
-    const int pct = (int)std::min<size_t>(100, (SVF_MINB_LP * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (smem > attr_smem[dev & 15]) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      // keep the L1 side large (in-flight gather lines), ask for just enough shared memory for the residency
+      const int pct = (int)std::min<size_t>(100, (SVF_MINB_LP * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      if (e != cudaSuccess) return e;
+      attr_smem[dev & 15] = smem;
+    }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSearchWarpsPerBlock * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;

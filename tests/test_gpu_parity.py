@@ -163,6 +163,23 @@ def test_large_pool_cache_sizing_paths_bit_exact(svf):
         assert np.array_equal(u32(ids), ri) and np.array_equal(f32(d), rd)
         cnt = idx.last_search_counters()
         assert cnt["iters"] == rc[:, 2].sum() and cnt["n_dist"] >= rc[:, 0].sum()
+    # a CUDA graph captured on the 6-block (larger) cache stays launchable after a 7-block launch of the same kernel
+    import torch
+
+    Qd = cuda(Q)
+    oi = torch.empty((5400, 10), dtype=torch.int32, device="cuda")
+    od = torch.empty((5400, 10), dtype=torch.float32, device="cuda")
+    idx.search_into(Qd, 10, 128, oi, od)
+    torch.cuda.synchronize()
+    g_ = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_):
+        idx.search_into(Qd, 10, 128, oi, od)
+    idx.search(cuda(Q[:300]), 10, 128)
+    oi.zero_()
+    g_.replay()
+    torch.cuda.synchronize()
+    ri, rd, _ = oracle.graph_search(X, g, Q, 10, 128, metric=1)
+    assert np.array_equal(u32(oi), ri) and np.array_equal(f32(od), rd)
 
 
 def test_two_new_vertices_in_one_sub_batch(svf):
