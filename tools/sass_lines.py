@@ -51,7 +51,7 @@ for (loc, txt), r in zip(seq, data):
     tot_s += s
     tot_e += e
 print(f"samples {tot_s}, instructions {tot_e}" + (f", per iteration {tot_e / iters:.1f}" if iters else ""))
-for loc, (s, e) in sorted(agg.items(), key=lambda x: -x[1][1 if "--by-inst" in sys.argv else 0])[:60]:
+for loc, (s, e) in sorted(agg.items(), key=lambda x: -x[1][1 if "--by-inst" in sys.argv else 0])[:(400 if "--all" in sys.argv else 60)]:
     top = ",".join(f"{c}:{v / max(s, 1):.2f}" for c, v in why[loc].most_common(2))
     print(f"{loc:28s} stall {s / tot_s:6.3f}  inst {e / tot_e:6.3f}" + (f"  ({e / iters:6.1f}/iter)" if iters else "")
           + f"  {top}")
