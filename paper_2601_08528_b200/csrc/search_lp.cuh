@@ -30,6 +30,12 @@ namespace {
 #ifndef SVF_LP_QSMEM
 #define SVF_LP_QSMEM 1
 #endif
+// SVF_LP_WHOLE = 1: whole-warp rows at D = 200 (SVF_GATHER_W_LP / 2 rows per round); measured against teams of 16
+// lanes with 2 rows each: C4 itopk 192 11.84 -> 11.00 ms; at D = 128 the 8-lane teams stay (whole-warp: 2.01 vs
+// 1.89 ms for an itopk-128 4096-query batch), profiles/r02_lp_ab.json
+#ifndef SVF_LP_WHOLE
+#define SVF_LP_WHOLE 1
+#endif
 // per-warp shared memory: [visited cache M entries (u16 tags or u32 ids); the query row is staged here before the
 // cache is cleared | pool Lp u64 | survivor ids MP u32 | keys MP u64 (compacted in place by C.Update) | query slot
 // 2 u64 | parents 8 u32].  M need not be a power of two (slot = multiply-shift of a hashed id), so the launcher
@@ -40,8 +46,13 @@ struct LpLayout {
     const size_t cb = (size_t)M * (c16 ? 2 : 4), qb = (size_t)Dp * 4;
     return ((cb > qb ? cb : qb) + 15) & ~(size_t)15;
   }
-  __host__ __device__ size_t qs_off() const { return cache_bytes(); }  // SVF_LP_QSMEM: a resident query copy
-  __host__ __device__ size_t pool_off() const { return qs_off() + (SVF_LP_QSMEM ? (((size_t)Dp * 4 + 15) & ~(size_t)15) : 0); }
+  // SVF_LP_QSMEM: a resident query copy for the team gather (the whole-warp gather at D = 200 keeps the query in
+  // registers, so it stages the row through the cache region instead)
+  __host__ __device__ bool qs_resident() const { return SVF_LP_QSMEM && !(SVF_LP_WHOLE && Dp == 200); }
+  __host__ __device__ size_t qs_off() const { return cache_bytes(); }
+  __host__ __device__ size_t pool_off() const {
+    return qs_off() + (qs_resident() ? (((size_t)Dp * 4 + 15) & ~(size_t)15) : 0);
+  }
   __host__ __device__ size_t sid_off() const { return pool_off() + (size_t)Lp * 8; }
   __host__ __device__ size_t skey_off() const { return sid_off() + (size_t)MP * 4; }
   __host__ __device__ size_t misc_off() const { return skey_off() + (size_t)MP * 8; }
@@ -54,12 +65,6 @@ struct LpLayout {
 
 #ifndef SVF_GATHER_U_LP
 #define SVF_GATHER_U_LP 2
-#endif
-// SVF_LP_WHOLE = 1: whole-warp rows at D = 200 (SVF_GATHER_W_LP / 2 rows per round); measured against teams of 16
-// lanes with 2 rows each: C4 itopk 192 11.84 -> 11.00 ms; at D = 128 the 8-lane teams stay (whole-warp: 2.01 vs
-// 1.89 ms for an itopk-128 4096-query batch), profiles/r02_lp_ab.json
-#ifndef SVF_LP_WHOLE
-#define SVF_LP_WHOLE 1
 #endif
 #ifndef SVF_GATHER_W_LP
 #define SVF_GATHER_W_LP 8
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   const LpLayout lay{a.vc_slots, (a.L + 31) & ~31, MP, VB > 0, a.dq * 4};
   unsigned char* base = smem + (size_t)wib * lay.warp_bytes();
   // the query is staged in the cache region (then the cache is cleared), or kept in its own region (SVF_LP_QSMEM)
-  float4* qs = reinterpret_cast<float4*>(base + (SVF_LP_QSMEM ? lay.qs_off() : 0));
+  float4* qs = reinterpret_cast<float4*>(base + (lay.qs_resident() ? lay.qs_off() : 0));
   uint32_t* cache = reinterpret_cast<uint32_t*>(base);
   uint16_t* cache16 = reinterpret_cast<uint16_t*>(base);
   uint64_t* pool = reinterpret_cast<uint64_t*>(base + lay.pool_off());

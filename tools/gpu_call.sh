@@ -1,3 +1,4 @@
-O=gpurun_out/ae
+O=gpurun_out/af
 mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 > $O/gpu_tests.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 300 > $O/parity.log 2>&1
+timeout 900 python bench.py --config C4 --no-extra --no-cpu --no-insert --steps 20 --warmup 5 --itopk 192 --max-iter 288 > $O/c4.json 2> $O/c4.err
