@@ -106,6 +106,13 @@ __device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4
   }
 }
 
+// One lane pulls every 128-byte line of vector row `id` toward L2 (the lane that found the survivor, at filter time)
+__device__ __forceinline__ void prefetch_row_l2(const float4* __restrict__ vec4, uint32_t id, int DQ) {
+  const int rb = DQ * 16;
+  const uintptr_t r0 = reinterpret_cast<uintptr_t>(vec4 + (size_t)id * DQ);
+  for (uintptr_t p = r0 & ~(uintptr_t)127; p < r0 + rb; p += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Distances of the S ids sid[0..S) -> keys skey[0..S): teams of T lanes per vector, U vectors per team per round
 // (U * 32/T rows in flight per warp), coalesced 16-byte gathers, FFMA, xor-shuffle reduction.
 // PF (K-S-L): a key below `pf` (the best unparented pool key) makes its id the likely next parent, so the lane that
@@ -145,7 +152,7 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vec4 + (size_t)sid[s] * DQ), "r"(DQ * 16)
                  : "memory");
 #elif SVF_PREFETCH == 1
-  prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
+  if (!PF) prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);  // K-S-L prefetched every survivor's row at its filter
 #endif
   // the team geometry covers a row exactly at D = 96 / 128 (T * NV = DQ): rows load unconditionally (a slot past S
   // re-reads survivor 0's row, an L1 hit, and its key is never stored); other widths keep the per-lane guards

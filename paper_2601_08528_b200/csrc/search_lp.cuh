@@ -94,7 +94,8 @@ __device__ __forceinline__ void gather_keys_w(const SearchArgs& a, const uint32_
   const float4* __restrict__ vec4 = reinterpret_cast<const float4*>(a.vec);
   __syncwarp();
   // every 128-byte line of the later rows (an exact-size cp.async.bulk.prefetch.L2 per 800-byte row avoids the line
-  // overfetch but was slower: C4 10.52 vs 10.81 ms)
+  // overfetch but was slower: C4 10.52 vs 10.81 ms; prefetching each row at its filter, as the team gather does, was
+  // slower here too: 7-8 lines per lane, 9.84 -> 10.11 ms)
   prefetch_rows_l2(vec4, sid, U, S, DQT, lane);
   for (int base = 0; base < S; base += U) {
     float4 xv[U][NV];
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           if (keep) {
             sid[pos] = id;
             cache_pos(id, M, VB, TM, slot, tag);
+            if (!kLpWhole) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, a.dq);
           }
           // one writer per slot (the lowest lane), so the cache never sees two stores to one slot at once
           const unsigned peers = SVF_LP_ONE_WRITER
@@ -460,7 +462,12 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           ok = VB ? cache16[slot] != (uint16_t)tag : cache[slot] != tag;
         }
         const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (ok) sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+        if (ok) {
+          sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+          // the survivor's vector row toward L2 now, a filter round before the gather loads it (team gathers: C2
+          // itopk 128 4096 queries 1.281 -> 1.245 ms, 10K 2.84 -> 2.70 ms; C2G 2.21 -> 2.13 ms)
+          if (!kLpWhole) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+        }
         if (SVF_LP_ONE_WRITER) __syncwarp();  // every lane's cache read of this round before any write
         // one writer per slot (the lowest lane); ids colliding in a slot are all scored, the cache keeps one
         const unsigned peers = SVF_LP_ONE_WRITER
