@@ -94,6 +94,11 @@ constexpr int gather_u() {
 // Pull every 128-byte line of the rows sid[first..S) toward L2 (prefetch.global.L2: no registers, nothing to wait
 // for), so the gather rounds that load them later hit L2.  A row of DQ float4 spans up to DQ*16/128 + 1 lines when
 // DQ*16 is not a multiple of 128 (D = 200: 800-byte rows start anywhere on a 32-byte sector, 7-8 lines).
+// SVF_KS_FILTER_PF = 1: K-S prefetches each survivor's row at its filter (as K-S-L does) instead of at the gather;
+// measured slower for K-S (C2 headline 0.5593 -> 0.5621 ms, C3 0.989 -> 1.289 ms), so off
+#ifndef SVF_KS_FILTER_PF
+#define SVF_KS_FILTER_PF 0
+#endif
 __device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4, const uint32_t* sid, int first,
                                                  int S, int DQ, int lane) {
   const int rb = DQ * 16;
@@ -152,7 +157,8 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vec4 + (size_t)sid[s] * DQ), "r"(DQ * 16)
                  : "memory");
 #elif SVF_PREFETCH == 1
-  if (!PF) prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);  // K-S-L prefetched every survivor's row at its filter
+  // K-S-L (and K-S with SVF_KS_FILTER_PF) prefetched every survivor's row at its filter
+  if (!PF && !SVF_KS_FILTER_PF) prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
 #endif
   // the team geometry covers a row exactly at D = 96 / 128 (T * NV = DQ): rows load unconditionally (a slot past S
   // re-reads survivor 0's row, an L1 hit, and its key is never stored); other widths keep the per-lane guards
@@ -488,6 +494,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
           if (keep) {
             sid[mine + __popc(km & ((1u << lane) - 1u))] = id;
             hash_insert(tab, a.hbits, id);
+            if (SVF_KS_FILTER_PF) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
           }
           mine += __popc(km);
           running += __popc(m);
@@ -620,7 +627,10 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         if (ok) ok = !tomb_dead(a.tomb, id);
         if (ok) ok = hash_insert(tab, a.hbits, id);
         const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (ok) sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+        if (ok) {
+          sid[running + __popc(m & ((1u << lane) - 1u))] = id;
+          if (SVF_KS_FILTER_PF) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+        }
         running += __popc(m);
       }
       SVF_PH(2)

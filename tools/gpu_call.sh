@@ -1,6 +1,11 @@
-O=gpurun_out/ah
+O=gpurun_out/ai
 mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 300 > $O/parity.log 2>&1
-timeout 600 python tools/pool_probe.py --itopks 128 --batches 4096,10000 --no-trace --out $O/c2.json > $O/c2.log 2>&1
-timeout 600 python bench.py --config C2G --no-extra --no-cpu --no-insert --steps 50 --warmup 10 --itopk 96 --max-iter 120 > $O/c2g.json 2> $O/c2g.err
-timeout 900 python bench.py --config C4 --no-extra --no-cpu --no-insert --steps 20 --warmup 5 --itopk 192 --max-iter 288 > $O/c4.json 2> $O/c4.err
+timeout 600 env SVF_LIB=paper_2601_08528_b200/libsvf_kspf.so python -m pytest tests/test_gpu_parity.py -q -x --timeout 300 -k "search or handoff or forget" > $O/parity.log 2>&1
+for v in main kspf main2 kspf2; do
+  L=paper_2601_08528_b200/libsvf.so; case $v in kspf*) L=paper_2601_08528_b200/libsvf_kspf.so;; esac
+  SVF_LIB=$L timeout 600 python bench.py --config C2 --no-extra --no-cpu --no-insert --steps 100 --warmup 10 --itopk 10 --max-iter 16 > $O/c2_$v.json 2> $O/c2_$v.err
+done
+for v in main kspf; do
+  L=paper_2601_08528_b200/libsvf.so; case $v in kspf*) L=paper_2601_08528_b200/libsvf_kspf.so;; esac
+  SVF_LIB=$L timeout 900 python bench.py --config C3 --no-extra --no-cpu --no-insert --steps 50 --warmup 10 --itopk 20 --max-iter 35 > $O/c3_$v.json 2> $O/c3_$v.err
+done
