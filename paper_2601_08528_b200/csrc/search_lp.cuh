@@ -27,6 +27,9 @@ namespace {
 // SVF_LP_QSMEM = 1: the team gather (D = 96 / 128) reads the query from a shared-memory copy instead of 4 float4
 // registers per lane, which removes the spills at the 72-register cap (C2 itopk 128: 4096 queries 1.438 -> 1.412 ms,
 // 10K 3.057 -> 3.017 ms; itopk 96 10K 2.474 -> 2.428 ms; profiles/r02_lp_ab.json)
+#ifndef SVF_LP_FILTER_PF
+#define SVF_LP_FILTER_PF 1
+#endif
 #ifndef SVF_LP_QSMEM
 #define SVF_LP_QSMEM 1
 #endif
@@ -184,6 +187,10 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   // whole-warp rows (gather_keys_w) at D = 200 (Geo<50> teams of 16 lanes leave 14 of 64 float4 slots idle and hold
   // 4 query float4 per lane); teams of Geo<DQT>::T lanes otherwise (D = 96 / 128: 8 lanes, no idle slots)
   constexpr bool kLpWhole = SVF_LP_WHOLE && DQT == 50;
+  // survivors' rows prefetched at the filter instead of at the gather (SVF_LP_FILTER_PF), at D = 128 only: measured
+  // faster there (C2 itopk 128 4096 q 1.277 -> 1.226 ms, C2G 2.21 -> 2.13 ms) but slower at D = 96 (C3 100K inserts
+  // 51.1 -> 58.7 ms of insert search) and D = 200 (C4 9.84 -> 10.11 ms)
+  constexpr bool kLpFilterPf = SVF_LP_FILTER_PF && DQT == 32;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int VB = a.vc_bits;  // 16-bit tagged cache when > 0
   const uint32_t M = (uint32_t)a.vc_slots, TM = a.vc_tmask;
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           if (keep) {
             sid[pos] = id;
             cache_pos(id, M, VB, TM, slot, tag);
-            if (!kLpWhole) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, a.dq);
+            if (kLpFilterPf) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, a.dq);
           }
           // one writer per slot (the lowest lane), so the cache never sees two stores to one slot at once
           const unsigned peers = SVF_LP_ONE_WRITER
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           sid[running + __popc(m & ((1u << lane) - 1u))] = id;
           // the survivor's vector row toward L2 now, a filter round before the gather loads it (team gathers: C2
           // itopk 128 4096 queries 1.281 -> 1.245 ms, 10K 2.84 -> 2.70 ms; C2G 2.21 -> 2.13 ms)
-          if (!kLpWhole) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+          if (kLpFilterPf) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
         }
         if (SVF_LP_ONE_WRITER) __syncwarp();  // every lane's cache read of this round before any write
         // one writer per slot (the lowest lane); ids colliding in a slot are all scored, the cache keeps one
