@@ -115,10 +115,17 @@ __device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4
 }
 
 // One lane pulls every 128-byte line of vector row `id` toward L2 (the lane that found the survivor, at filter time)
+template <int DQT>
 __device__ __forceinline__ void prefetch_row_l2(const float4* __restrict__ vec4, uint32_t id, int DQ) {
-  const int rb = DQ * 16;
-  const uintptr_t r0 = reinterpret_cast<uintptr_t>(vec4 + (size_t)id * DQ);
-  for (uintptr_t p = r0 & ~(uintptr_t)127; p < r0 + rb; p += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  if constexpr (DQT > 0 && (DQT * 16) % 128 == 0) {  // rows are whole, aligned lines (D = 128: 4): unrolled
+    const char* r0 = reinterpret_cast<const char*>(vec4 + (size_t)id * DQT);
+#pragma unroll
+    for (int j = 0; j < DQT * 16 / 128; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + j * 128));
+  } else {
+    const int rb = DQ * 16;
+    const uintptr_t r0 = reinterpret_cast<uintptr_t>(vec4 + (size_t)id * DQ);
+    for (uintptr_t p = r0 & ~(uintptr_t)127; p < r0 + rb; p += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
 }
 
 // Distances of the S ids sid[0..S) -> keys skey[0..S): teams of T lanes per vector, U vectors per team per round
@@ -497,7 +504,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
           if (keep) {
             sid[mine + __popc(km & ((1u << lane) - 1u))] = id;
             hash_insert(tab, a.hbits, id);
-            if (SVF_KS_FILTER_PF) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+            if (SVF_KS_FILTER_PF) prefetch_row_l2<DQT>(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
           }
           mine += __popc(km);
           running += __popc(m);
@@ -632,7 +639,7 @@ __device__ __forceinline__ void run_queries(const SearchArgs& a, unsigned char* 
         const unsigned m = __ballot_sync(0xffffffffu, ok);
         if (ok) {
           sid[running + __popc(m & ((1u << lane) - 1u))] = id;
-          if (SVF_KS_FILTER_PF) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+          if (SVF_KS_FILTER_PF) prefetch_row_l2<DQT>(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
         }
         running += __popc(m);
       }

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           if (keep) {
             sid[pos] = id;
             cache_pos(id, M, VB, TM, slot, tag);
-            if (kLpFilterPf) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, a.dq);
+            if (kLpFilterPf) prefetch_row_l2<DQT>(reinterpret_cast<const float4*>(a.vec), id, a.dq);
           }
           // one writer per slot (the lowest lane), so the cache never sees two stores to one slot at once
           const unsigned peers = SVF_LP_ONE_WRITER
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
           sid[running + __popc(m & ((1u << lane) - 1u))] = id;
           // the survivor's vector row toward L2 now, a filter round before the gather loads it (team gathers: C2
           // itopk 128 4096 queries 1.281 -> 1.245 ms, 10K 2.84 -> 2.70 ms; C2G 2.21 -> 2.13 ms)
-          if (kLpFilterPf) prefetch_row_l2(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
+          if (kLpFilterPf) prefetch_row_l2<DQT>(reinterpret_cast<const float4*>(a.vec), id, DQT ? DQT : a.dq);
         }
         if (SVF_LP_ONE_WRITER) __syncwarp();  // every lane's cache read of this round before any write
         // one writer per slot (the lowest lane); ids colliding in a slot are all scored, the cache keeps one
