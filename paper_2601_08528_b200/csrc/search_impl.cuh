@@ -102,6 +102,9 @@ constexpr int gather_u() {
 #ifndef SVF_LP_FILTER_PF
 #define SVF_LP_FILTER_PF 1
 #endif
+#ifndef SVF_LP_FILTER_PF96
+#define SVF_LP_FILTER_PF96 0
+#endif
 __device__ __forceinline__ void prefetch_rows_l2(const float4* __restrict__ vec4, const uint32_t* sid, int first,
                                                  int S, int DQ, int lane) {
   const int rb = DQ * 16;
@@ -168,7 +171,8 @@ __device__ __forceinline__ void gather_keys(const SearchArgs& a, const uint32_t*
                  : "memory");
 #elif SVF_PREFETCH == 1
   // K-S-L (and K-S with SVF_KS_FILTER_PF) prefetched every survivor's row at its filter
-  if (PF ? !(SVF_LP_FILTER_PF && DQT == 32) : !SVF_KS_FILTER_PF) prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
+  if (PF ? !(SVF_LP_FILTER_PF && (DQT == 32 || (SVF_LP_FILTER_PF96 && DQT == 24))) : !SVF_KS_FILTER_PF)
+    prefetch_rows_l2(vec4, sid, nteams * U, S, DQ, lane);
 #endif
   // the team geometry covers a row exactly at D = 96 / 128 (T * NV = DQ): rows load unconditionally (a slot past S
   // re-reads survivor 0's row, an L1 hit, and its key is never stored); other widths keep the per-lane guards

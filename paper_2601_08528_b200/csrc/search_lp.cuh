@@ -30,6 +30,11 @@ namespace {
 #ifndef SVF_LP_FILTER_PF
 #define SVF_LP_FILTER_PF 1
 #endif
+// SVF_LP_FILTER_PF96 = 1 extends it to D = 96 (unrolled 3 lines): still slower there (C3 100K inserts, insert search
+// 51.1 -> 55.9 ms)
+#ifndef SVF_LP_FILTER_PF96
+#define SVF_LP_FILTER_PF96 0
+#endif
 #ifndef SVF_LP_QSMEM
 #define SVF_LP_QSMEM 1
 #endif
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
   // survivors' rows prefetched at the filter instead of at the gather (SVF_LP_FILTER_PF), at D = 128 only: measured
   // faster there (C2 itopk 128 4096 q 1.277 -> 1.226 ms, C2G 2.21 -> 2.13 ms) but slower at D = 96 (C3 100K inserts
   // 51.1 -> 58.7 ms of insert search) and D = 200 (C4 9.84 -> 10.11 ms)
-  constexpr bool kLpFilterPf = SVF_LP_FILTER_PF && DQT == 32;
+  constexpr bool kLpFilterPf = SVF_LP_FILTER_PF && (DQT == 32 || (SVF_LP_FILTER_PF96 && DQT == 24));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int VB = a.vc_bits;  // 16-bit tagged cache when > 0
   const uint32_t M = (uint32_t)a.vc_slots, TM = a.vc_tmask;
