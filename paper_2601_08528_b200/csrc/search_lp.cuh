@@ -174,6 +174,31 @@ __device__ __forceinline__ void cache_pos(uint32_t id, uint32_t M, int B, uint32
   }
 }
 
+// the same, with the quartile keys of a[0..n) read together first (three independent broadcast reads instead of two
+// dependent probes), then a binary search inside the quarter
+__device__ __forceinline__ int lower_bound_key_q(const uint64_t* a, int n, uint64_t k) {
+  int lo = 0, hi = n;
+  if (n >= 16) {
+    const int q1 = n >> 2, q2 = n >> 1, q3 = q1 + q2;
+    const uint64_t f1 = a[q1] & ~1ull, f2 = a[q2] & ~1ull, f3 = a[q3] & ~1ull;
+    if (f2 < k) {
+      lo = q2 + 1;
+      if (f3 < k) lo = q3 + 1;
+      else hi = q3;
+    } else {
+      hi = q2;
+      if (f1 < k) lo = q1 + 1;
+      else hi = q1;
+    }
+  }
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((a[mid] & ~1ull) < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // number of keys in sorted a[0..n) whose flag-stripped value is < k (k has its flag bit clear)
 __device__ __forceinline__ int lower_bound_key(const uint64_t* a, int n, uint64_t k) {
   int lo = 0, hi = n;
@@ -299,7 +324,7 @@ __global__ void __launch_bounds__(kSearchWarpsPerBlock * 32, SVF_MINB_LP) search
         int b = L;
         bool keep = false;
         if (lane < nh) {
-          b = lower_bound_key(pool, np, c);
+          b = lower_bound_key_q(pool, np, c);
           keep = !(b < np && (pool[b] & ~1ull) == c);  // already in the pool (the cache forgot it)
         }
         // the same id offered twice (p > 1): keep the first copy (lanes >= nh hold kEmptyKey and keep = false)

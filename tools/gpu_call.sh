@@ -1,6 +1,6 @@
 # final round-2 evidence: GPU tests, smoke, default bench, reference arm, N=2 plumbing (gloo, one device),
 # and ncu (--set full + launch lists) of every default-bench search launch and of one 10K insert into C2
-O=gpurun_out/fin4
+O=gpurun_out/fin5
 mkdir -p $O
 (time timeout 2400 python -m pytest tests -m gpu -q -rf --timeout 900) > $O/gpu_tests.log 2>&1
 (time timeout 300 python -c "import __graft_entry__ as g; g.smoke()") > $O/smoke.log 2>&1
